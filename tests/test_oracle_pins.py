@@ -1,0 +1,422 @@
+"""Pins for the CPU oracle (oracle/oracle.c) against things other than itself.
+
+Each test cites what fixes the expected value: the paper (Table 1, §2 claims), the plain
+definition via brute force over subsets (tests/brute.py), closed forms, invariants, or
+published reference outputs.  CPU only (``-m "not gpu"``).
+"""
+import itertools
+import math
+import os
+
+import numpy as np
+import pytest
+
+import oracle
+from paper_1410_4876_b200 import inputs as I
+from tests import brute
+
+GOLDEN = os.path.join(os.path.dirname(__file__), "golden")
+
+
+def _sets(cycles):
+    return {frozenset(c) for c in cycles}
+
+
+# ------------------------------------------------------------------------- hash primitive
+def test_mix_matches_published_splitmix64_sequence():
+    """SplitMix64 (Steele, Lea & Flood 2014; java.util.SplittableRandom) seeded with 0
+    outputs e220a8397b1dcdaf, 6e789e6aa1b965f4, 06c45d188009454f: output i is the
+    finaliser applied to i*golden, i.e. mix((i-1)*golden) with our mix adding golden."""
+    g = 0x9E3779B97F4A7C15
+    assert oracle.mix(0) == 0xE220A8397B1DCDAF
+    assert oracle.mix(g) == 0x6E789E6AA1B965F4
+    assert oracle.mix((2 * g) & brute.M64) == 0x06C45D188009454F
+
+
+# ------------------------------------------------------------------------- brute force
+def _random_graphs():
+    out = []
+    for n in (4, 6, 8, 10, 12):
+        for p in (0.2, 0.35, 0.5):
+            for seed in range(4):
+                out.append((f"gnp{n}_{p}_{seed}", I.gnp(n, p, 1000 * n + int(100 * p) + seed)))
+    return out
+
+
+SMALL = [
+    ("p4x4", I.grid(4, 4)), ("p3x5", I.grid(3, 5)), ("k3x4", I.complete_bipartite(3, 4)),
+    ("k5", I.complete(5)), ("c7", I.cycle(7)), ("w6", I.wheel(6)), ("w3", I.wheel(3)),
+    ("fig1", I.fig1_graph()), ("path5", I.path(5)), ("star4", I.star(4)),
+    ("tree10", I.random_tree(10, 3)), ("empty", I.edges_to_csr(5, [])),
+] + _random_graphs()
+
+
+@pytest.mark.parametrize("name,g", SMALL, ids=[s[0] for s in SMALL])
+def test_oracle_equals_brute_force_sets_counts_and_hash(name, g):
+    """Definition: the cycle set equals every S with G[S] connected 2-regular.
+    Exactly once: no duplicate vertex sets in the oracle's list."""
+    n, rp, col = g
+    want = brute.chordless_cycles_brute(n, rp, col)
+    r = oracle.enumerate_cycles(n, rp, col, collect=True)
+    got = [frozenset(c) for c in r["cycles"]]
+    assert len(got) == len(set(got)), "a cycle was emitted twice"
+    assert set(got) == want
+    assert r["counts"].tolist() == brute.counts_of(want, n)
+    assert r["set_hash"] == brute.hspec_hash(want)
+
+
+def test_hash_seed_changes_hash_but_not_counts():
+    n, rp, col = I.grid(4, 4)
+    a = oracle.enumerate_cycles(n, rp, col)
+    b = oracle.enumerate_cycles(n, rp, col, seed=12345)
+    want = brute.chordless_cycles_brute(n, rp, col)
+    assert b["set_hash"] == brute.hspec_hash(want, seed=12345)
+    assert a["set_hash"] != b["set_hash"]
+    assert (a["counts"] == b["counts"]).all()
+
+
+# ------------------------------------------------------------------------- closed forms
+@pytest.mark.parametrize("k", range(3, 13))
+def test_cycle_graph_has_one_chordless_cycle(k):
+    """C_k has exactly one chordless cycle (PAPER.md:409 for k=100)."""
+    r = oracle.enumerate_cycles(*I.cycle(k))
+    assert int(r["counts"].sum()) == 1 and int(r["counts"][k]) == 1
+    # |T| = 1 for a unique cycle of length >= 4, 0 for a triangle (reading G11)
+    t, ntri = oracle.triplets(*I.cycle(k))
+    assert (len(t), ntri) == ((1, 0) if k >= 4 else (0, 1))
+
+
+@pytest.mark.parametrize("k", range(3, 10))
+def test_complete_graph_has_only_triangles(k):
+    """K_k: C(k,3) triangles and nothing longer (any 4 vertices have a chord)."""
+    r = oracle.enumerate_cycles(*I.complete(k))
+    assert int(r["counts"][3]) == math.comb(k, 3)
+    assert int(r["counts"].sum()) == math.comb(k, 3)
+
+
+@pytest.mark.parametrize("a,b", [(1, 5), (2, 2), (2, 5), (3, 3), (4, 6), (6, 6), (5, 3)])
+def test_complete_bipartite_closed_form(a, b):
+    """K_{a,b}: C(a,2)*C(b,2) chordless cycles, all of length 4."""
+    r = oracle.enumerate_cycles(*I.complete_bipartite(a, b))
+    assert int(r["counts"][4]) == math.comb(a, 2) * math.comb(b, 2)
+    assert int(r["counts"].sum()) == math.comb(a, 2) * math.comb(b, 2)
+
+
+@pytest.mark.parametrize("a", [2, 3, 8, 20, 50])
+def test_kaa_stage_sizes_under_degree_labelling(a):
+    """K_{a,a} with lowest-id ties: |F_3| = C(a+1,3) + C(a,3) and F_4 empty;
+    candidates = a * |F_3| (every triplet scans the a neighbours of y)."""
+    r = oracle.enumerate_cycles(*I.complete_bipartite(a, a))
+    f3 = math.comb(a + 1, 3) + math.comb(a, 3)
+    assert int(r["paths_by_len"][3]) == f3
+    assert int(r["paths_by_len"].sum()) == f3
+    assert r["candidates"] == a * f3
+
+
+@pytest.mark.parametrize("k", range(3, 14))
+def test_wheel_closed_form(k):
+    """W_k: k triangles plus the rim k-cycle for k >= 4; W_3 = K_4."""
+    r = oracle.enumerate_cycles(*I.wheel(k))
+    if k == 3:
+        assert int(r["counts"][3]) == 4 and int(r["counts"].sum()) == 4
+    else:
+        assert int(r["counts"][3]) == k
+        assert int(r["counts"][k]) == 1
+        assert int(r["counts"].sum()) == k + 1
+
+
+@pytest.mark.parametrize("seed", range(5))
+def test_trees_have_no_triplets_and_no_cycles(seed):
+    """A tree has T(G) = empty for any labelling."""
+    g = I.random_tree(30, seed)
+    t, ntri = oracle.triplets(*g)
+    assert len(t) == 0 and ntri == 0
+    assert int(oracle.enumerate_cycles(*g)["counts"].sum()) == 0
+
+
+def test_unicyclic_graph_has_one_triplet():
+    """A unique cycle (length >= 4) gives |T(G)| = 1 for any degree labelling."""
+    # C_6 with pendant trees
+    edges = [(i, (i + 1) % 6) for i in range(6)] + [(0, 6), (6, 7), (3, 8), (8, 9), (8, 10)]
+    g = I.edges_to_csr(11, edges)
+    t, ntri = oracle.triplets(*g)
+    assert len(t) == 1 and ntri == 0
+    r = oracle.enumerate_cycles(*g)
+    assert int(r["counts"][6]) == 1 and int(r["counts"].sum()) == 1
+
+
+# ------------------------------------------------------------------------- Table 1
+def _table1_rows():
+    rows = []
+    with open(os.path.join(GOLDEN, "table1_counts.txt")) as f:
+        for line in f:
+            line = line.split("#")[0].strip()
+            if not line:
+                continue
+            name, fam, par, n, m, d, c3, clc = line.split()
+            rows.append((name, fam, par, int(n), int(m), int(d), int(c3), int(clc)))
+    return rows
+
+
+def _family(fam, par):
+    if fam == "cycle":
+        return I.cycle(int(par))
+    if fam == "wheel":
+        return I.wheel(int(par))
+    a, b = (int(x) for x in par.split(","))
+    return I.complete_bipartite(a, b) if fam == "bipartite" else I.grid(a, b)
+
+
+_FAST = {"C_100", "Wheel_100", "K_8_8", "K_50_50", "Grid_4x10", "Grid_5x6", "Grid_5x10",
+         "Grid_6x6", "Grid_6x10", "Grid_7x10"}
+
+
+@pytest.mark.parametrize("row", _table1_rows(), ids=lambda r: r[0])
+def test_table1_counts(row):
+    """Table 1: n, m, Delta, C3 and #clc of the synthetic graphs."""
+    name, fam, par, n, m, d, c3, clc = row
+    if name not in _FAST and os.environ.get("CC_SLOW") != "1":
+        pytest.skip("slow tier (CC_SLOW=1)")
+    g = _family(fam, par)
+    assert g[0] == n
+    assert len(g[2]) == 2 * m
+    assert int(np.diff(g[1]).max()) == d
+    r = oracle.enumerate_cycles(*g, nthreads=os.cpu_count() or 1)
+    assert int(r["counts"][3]) == c3
+    assert int(r["counts"][4:].sum()) == clc
+
+
+def test_grid7x10_frontier_peak_matches_paper():
+    """Grid 7x10 peaks at "14 millions of chordless paths stored".
+    Our |F_t| peak (lowest-id ties) must be 14 M to two significant figures."""
+    r = oracle.enumerate_cycles(*I.grid(7, 10), nthreads=os.cpu_count() or 1)
+    peak = int(r["paths_by_len"].max())
+    assert 13_500_000 <= peak < 14_500_000
+    # the evolution is a wave: rises from |F_3| then falls to 0
+    f = r["paths_by_len"]
+    t_peak = int(np.argmax(f))
+    assert f[3] < peak and t_peak > 3 and int(f[-1]) == 0
+
+
+# ------------------------------------------------------------------------- grid formulas
+def _grid_totals():
+    rows = []
+    with open(os.path.join(GOLDEN, "grid_closed_forms.txt")) as f:
+        for line in f:
+            line = line.split("#")[0].strip()
+            if line:
+                fam, ncol, total = line.split()
+                rows.append((int(fam[1]), int(ncol), int(total)))
+    return rows
+
+
+@pytest.mark.parametrize("r,c,total", _grid_totals())
+def test_grid_totals_hand_derived(r, c, total):
+    assert int(oracle.enumerate_cycles(*I.grid(r, c))["counts"].sum()) == total
+
+
+@pytest.mark.parametrize("c", range(2, 12))
+def test_grid_two_and_three_rows(c):
+    """P2xPn = n-1, P3xPn = 2(n-1) + C(n-1,2)."""
+    assert int(oracle.enumerate_cycles(*I.grid(2, c))["counts"].sum()) == c - 1
+    assert int(oracle.enumerate_cycles(*I.grid(3, c))["counts"].sum()) == 2 * (c - 1) + math.comb(c - 1, 2)
+
+
+def _n_len(r, c):
+    z = lambda x: max(x, 0)
+    return {
+        4: z(r - 1) * z(c - 1),
+        6: 0,
+        8: z(r - 2) * z(c - 2),
+        10: z(r - 2) * z(c - 3) + z(r - 3) * z(c - 2),
+        12: 7 * z(r - 3) * z(c - 3) + z(r - 2) * z(c - 4) + z(r - 4) * z(c - 2),
+    }
+
+
+@pytest.mark.parametrize("r,c", [(4, 4), (5, 5), (6, 6), (4, 7), (6, 8), (7, 7)])
+def test_grid_short_length_histogram(r, c):
+    """N4..N12 closed forms and zero odd lengths (bipartite) for any grid."""
+    counts = oracle.enumerate_cycles(*I.grid(r, c), nthreads=os.cpu_count() or 1)["counts"]
+    for k, v in _n_len(r, c).items():
+        assert int(counts[k]) == v, k
+    assert int(counts[1::2].sum()) == 0
+
+
+def test_p4x4_full_histogram():
+    """BASELINE configs[0]: P4xP4 = {4:9, 8:4, 10:4, 12:7}."""
+    c = oracle.enumerate_cycles(*I.grid(4, 4))["counts"]
+    assert {k: int(v) for k, v in enumerate(c) if v} == {4: 9, 8: 4, 10: 4, 12: 7}
+
+
+# ------------------------------------------------------------------------- labelling
+def _replay_ok(n, rp, col, labels):
+    """Replay property: deleting vertices in label order, each deleted
+    vertex has minimum degree in the remaining graph."""
+    adj = brute.adjacency_sets(n, rp, col)
+    order = np.argsort(labels)
+    alive = set(range(n))
+    deg = {v: len(adj[v]) for v in range(n)}
+    for u in order:
+        u = int(u)
+        if deg[u] != min(deg[v] for v in alive):
+            return False
+        alive.remove(u)
+        for w in adj[u]:
+            if w in alive:
+                deg[w] -= 1
+    return True
+
+
+@pytest.mark.parametrize("name,g", SMALL[:12] + [("k150", I.complete_bipartite(20, 30)),
+                                                  ("g8x8", I.grid(8, 8)), ("gnp", I.gnp(60, 0.1, 7))])
+def test_degree_labelling_replay_and_bijection(name, g):
+    n, rp, col = g
+    lab = oracle.degree_labeling(n, rp, col)
+    assert sorted(lab.tolist()) == list(range(n))
+    assert _replay_ok(n, rp, col, lab)
+
+
+def test_degree_labelling_tie_break_examples():
+    """Lowest-id tie-break (reading G1; SPEC.md:143-145 examples)."""
+    assert oracle.degree_labeling(*I.path(3)).tolist() == [0, 1, 2]
+    assert oracle.degree_labeling(*I.complete(3)).tolist() == [0, 1, 2]
+    # K_{1,4}, hub 0: leaves 1,2,3 go first (degree 1 < hub); then hub and leaf 4 both
+    # have degree 1 and the lower id (the hub) wins.  (SPEC.md:145 says the hub is last;
+    # that ignores the final tie -- derived by hand here.)
+    assert oracle.degree_labeling(*I.star(4)).tolist() == [3, 0, 1, 2, 4]
+    # K_{a,a}: A0, B0, A1, B1, ...
+    lab = oracle.degree_labeling(*I.complete_bipartite(4, 4))
+    assert lab.tolist() == [0, 2, 4, 6, 1, 3, 5, 7]
+
+
+# ------------------------------------------------------------------------- triplets
+@pytest.mark.parametrize("name,g", SMALL + [("g8x8", I.grid(8, 8)), ("k10", I.complete_bipartite(10, 7))])
+def test_triplet_definition_and_bound(name, g):
+    """T(G): x,y in Adj(u), l(u) < l(x) < l(y), (x,y) not in E; and the
+    bound |T(G)| <= (Delta-1) m / 2.  Rechecked here by brute force over (u, x, y)."""
+    n, rp, col = g
+    adj = brute.adjacency_sets(n, rp, col)
+    lab = oracle.degree_labeling(n, rp, col)
+    t, ntri = oracle.triplets(n, rp, col)
+    want_t, want_c = set(), 0
+    for u in range(n):
+        for x in adj[u]:
+            for y in adj[u]:
+                if lab[u] < lab[x] < lab[y]:
+                    if y in adj[x]:
+                        want_c += 1
+                    else:
+                        want_t.add((x, u, y))
+    assert {tuple(r) for r in t.tolist()} == want_t
+    assert ntri == want_c
+    m = len(col) // 2
+    delta = int(np.diff(rp).max()) if n else 0
+    assert len(t) <= (delta - 1) * m / 2 + 1e-9 or len(t) == 0
+
+
+def test_paper_worked_example_stage1():
+    """with l(u=0)=0, l(x=1)=1, l(y=3)=14 and x, y non-adjacent,
+    <1,0,3> is an initial valid triplet (the rule l(u) < l(x) < l(y), reading G4).
+    Fig. 1 adjacency: 0 ~ {1,3}, 1 ~ {0,2,4}."""
+    edges = [(0, 1), (0, 3), (1, 2), (1, 4)] + [(i, i + 1) for i in range(4, 15)]
+    n, rp, col = I.edges_to_csr(16, edges)
+    lab = np.arange(16, dtype=np.int32)
+    lab[3], lab[14] = 14, 3  # l(3) = 14
+    t, _ = oracle.triplets(n, rp, col, labels=lab)
+    assert (1, 0, 3) in {tuple(r) for r in t.tolist()}
+
+
+# ------------------------------------------------------------------------- canonical form
+@pytest.mark.parametrize("name,g", SMALL[:14])
+def test_cycles_are_canonical_and_induced(name, g):
+    """Each output <v1..vk> is a cycle of G, induced (|E(G[S])| = k), and canonical:
+    l(v2) = min over the cycle and l(v1) < l(v3)."""
+    n, rp, col = g
+    adj = brute.adjacency_sets(n, rp, col)
+    lab = oracle.degree_labeling(n, rp, col)
+    for c in oracle.enumerate_cycles(n, rp, col, collect=True)["cycles"]:
+        k = len(c)
+        assert len(set(c)) == k >= 3
+        for i in range(k):
+            assert c[(i + 1) % k] in adj[c[i]]
+        S = set(c)
+        assert sum(len(adj[v] & S) for v in S) == 2 * k
+        assert lab[c[1]] == min(lab[v] for v in c)
+        assert lab[c[0]] < lab[c[2]]
+
+
+# ------------------------------------------------------------------------- metamorphic
+@pytest.mark.parametrize("seed", range(6))
+def test_any_labelling_gives_the_same_cycle_set(seed):
+    """Any bijection l defines each cycle uniquely, so Alg. 1 with an
+    arbitrary labelling returns the same set, counts and hash; |F_t| may change."""
+    n, rp, col = I.gnp(14, 0.3, 77 + seed) if seed % 2 else I.grid(4, 5)
+    rng = np.random.default_rng(seed)
+    lab = rng.permutation(n).astype(np.int32)
+    a = oracle.enumerate_cycles(n, rp, col, collect=True)
+    b = oracle.enumerate_cycles(n, rp, col, labels=lab, collect=True)
+    assert _sets(a["cycles"]) == _sets(b["cycles"])
+    assert a["set_hash"] == b["set_hash"]
+    assert (a["counts"] == b["counts"]).all()
+
+
+@pytest.mark.parametrize("seed", range(4))
+def test_vertex_permutation_maps_cycles(seed):
+    """Renaming vertices maps the cycle set through the renaming (isomorphism invariance)."""
+    n, rp, col = I.gnp(16, 0.25, 500 + seed) if seed else I.grid(4, 4)
+    perm = np.random.default_rng(seed).permutation(n)
+    g2 = I.permute(n, rp, col, perm)
+    a = _sets(oracle.enumerate_cycles(n, rp, col, collect=True)["cycles"])
+    b = _sets(oracle.enumerate_cycles(*g2, collect=True)["cycles"])
+    assert {frozenset(int(perm[v]) for v in S) for S in a} == b
+
+
+# ------------------------------------------------------------------------- max_len, sampling
+@pytest.mark.parametrize("K", [3, 4, 5, 8, 10])
+def test_max_len_truncates_exactly(K):
+    """Reading G14: with a cap K the counts are the full counts for k <= K, zero above;
+    a path of t vertices is scanned iff t + 1 <= K."""
+    n, rp, col = I.grid(5, 6)
+    full = oracle.enumerate_cycles(n, rp, col)
+    cap = oracle.enumerate_cycles(n, rp, col, max_len=K)
+    assert cap["counts"][:K + 1].tolist() == full["counts"][:K + 1].tolist()
+    assert int(cap["counts"][K + 1:].sum()) == 0
+    assert cap["paths_by_len"][:K].tolist() == full["paths_by_len"][:K].tolist()
+    assert int(cap["paths_by_len"][K:].sum()) == 0
+
+
+def test_root_sampling_partitions_the_roots():
+    """Root samples (offset 0..s-1) partition T(G): their counts and hashes sum to the
+    full run; triangles are counted only by offset 0."""
+    n, rp, col = I.gnp(40, 0.15, 3)
+    full = oracle.enumerate_cycles(n, rp, col)
+    s = 5
+    parts = [oracle.enumerate_cycles(n, rp, col, root_stride=s, root_offset=o) for o in range(s)]
+    assert sum(p["counts"] for p in parts).tolist() == full["counts"].tolist()
+    assert sum(p["set_hash"] for p in parts) % (1 << 64) == full["set_hash"]
+    assert sum(p["paths_by_len"] for p in parts).tolist() == full["paths_by_len"].tolist()
+
+
+def test_threads_do_not_change_results():
+    g = I.grid(6, 6)
+    a = oracle.enumerate_cycles(*g, nthreads=1)
+    b = oracle.enumerate_cycles(*g, nthreads=7)
+    assert a["counts"].tolist() == b["counts"].tolist()
+    assert a["set_hash"] == b["set_hash"]
+    assert a["paths_by_len"].tolist() == b["paths_by_len"].tolist()
+    assert a["candidates"] == b["candidates"]
+
+
+# ------------------------------------------------------------------------- validation
+def test_csr_validation_error_kinds():
+    """out-of-range id, self-loop, asymmetric pair are errors; duplicates merge."""
+    rp = np.array([0, 1, 2], dtype=np.int64)
+    assert oracle.validate(2, rp, np.array([1, 0], dtype=np.int32)) == "OK"
+    assert oracle.validate(2, rp, np.array([2, 0], dtype=np.int32)) == "INVALID_VERTEX"
+    assert oracle.validate(2, rp, np.array([0, 0], dtype=np.int32)) == "SELF_LOOP"
+    assert oracle.validate(3, np.array([0, 1, 1, 1]), np.array([1], dtype=np.int32)) == "NOT_SYMMETRIC"
+    # duplicates inside a row are merged: triangle with a doubled entry is still one triangle
+    rp = np.array([0, 3, 5, 7], dtype=np.int64)
+    col = np.array([1, 2, 1, 0, 2, 0, 1], dtype=np.int32)
+    r = oracle.enumerate_cycles(3, rp, col)
+    assert int(r["counts"][3]) == 1
