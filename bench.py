@@ -1,0 +1,336 @@
+#!/usr/bin/env python
+"""Benchmark of the chordless-cycle hot path (arXiv 1410.4876) on B200.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--workload NAME] [--impl ours|reference]
+
+A "step" is one whole enumeration (Stage 1 + every Stage-2 level) of
+the workload graph.  For N > 1 the driver launches one process per GPU with torchrun; each rank
+enumerates its shard (cc_options.shard_index/count) and the per-length counts + set hash are
+summed with one NCCL all_reduce (the only cross-GPU exchange).  Time is measured
+on the device with CUDA events and the max over ranks is taken.
+
+Prints ONE JSON line (rank 0).  See DESIGN.md "Measurement" for every field.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+if ROOT not in sys.path:
+    sys.path.insert(0, ROOT)
+
+from paper_1410_4876_b200 import inputs  # noqa: E402
+
+METRIC = "chordless cycles/sec and paths expanded/sec at 1/2/4/8 B200; HBM roofline %"
+UNIT = "cycles/s"
+
+# name -> (graph builder, max_len, description)
+WORKLOADS = {
+    "p10x10": (lambda: inputs.grid(10, 10), 0, "grid P10xP10 (BASELINE configs[4]), full enumeration"),
+    "k150": (lambda: inputs.complete_bipartite(150, 150), 0, "K_{150,150} (BASELINE configs[1])"),
+    "p8x8": (lambda: inputs.grid(8, 8), 0, "grid P8xP8 (BASELINE configs[2])"),
+    "p4x4": (lambda: inputs.grid(4, 4), 0, "grid P4xP4 (BASELINE configs[0])"),
+    "grid8x10": (lambda: inputs.grid(8, 10), 0, "grid P8xP10 (Table 1 row, PAPER.md:419)"),
+}
+DEFAULT_WORKLOAD = "p10x10"
+
+# oracle samples (bounded CPU work, ~10-30 s) for cpu_baseline / --impl reference
+ORACLE_SAMPLE = {
+    "p10x10": dict(max_len=26),
+    "k150": dict(),
+    "p8x8": dict(),
+    "p4x4": dict(),
+    "grid8x10": dict(max_len=30),
+}
+
+
+def peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            d = json.load(f)
+        return float(d["hbm_gbs"]), "measured"
+    except Exception:
+        return 6650.0, "fallback"
+
+
+class ClockSampler:
+    """nvidia-smi sampling during the timed region (B200_PROFILING.md clocks line)."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu_index: int):
+        self.gpu = gpu_index
+        self.proc = None
+        self.lines = []
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.gpu), f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
+                 "-lms", "100"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def __exit__(self, *a):
+        if self.proc:
+            time.sleep(0.25)
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        sm, smax, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            p = [x.strip() for x in ln.split(",")]
+            if len(p) < 8:
+                continue
+            try:
+                sm.append(float(p[0]))
+                smax.append(float(p[1]))
+            except ValueError:
+                continue
+            for name, val in zip(names, p[4:8]):
+                if val.lower() == "active":
+                    reasons.add(name)
+        if not sm:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"], "samples": 0}
+        return {"sm_mhz": float(np.median(sm)), "sm_max_mhz": max(smax), "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+def dist_env():
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", str(rank)))
+    return rank, world, local
+
+
+def oracle_sample(workload: str, g):
+    """Run the oracle on the bounded sample; returns (cycles, paths, seconds, cores, desc)."""
+    import oracle
+    kw = ORACLE_SAMPLE.get(workload, {})
+    cores = os.cpu_count() or 1
+    t0 = time.perf_counter()
+    r = oracle.enumerate_cycles(*g, nthreads=cores, **kw)
+    dt = time.perf_counter() - t0
+    desc = f"{workload}" + (f" with max_len={kw['max_len']}" if kw.get("max_len") else " (whole graph)")
+    desc += f", oracle (C, Alg. 1 DFS) on {cores} host threads, root-split"
+    return int(r["counts"].sum()), int(r["paths_by_len"].sum()), dt, cores, desc
+
+
+def run_reference(args, workload, g):
+    rank, world, _ = dist_env()
+    if rank != 0:
+        return 0
+    times, cyc, paths = [], 0, 0
+    desc = cores = None
+    for i in range(args.warmup + args.steps):
+        c, p, dt, cores, desc = oracle_sample(workload, g)
+        if i >= args.warmup:
+            times.append(dt)
+            cyc, paths = c, p
+    tot = sum(times)
+    value = cyc * len(times) / tot
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * tot / len(times),
+        "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "u64",
+        "data": "synthetic", "config": {"workload": workload, "sample": desc},
+        "paths_per_s": paths * len(times) / tot,
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "oracle", "sample": desc},
+        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--workload", default=DEFAULT_WORKLOAD, choices=sorted(WORKLOADS))
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--workspace-gb", type=float, default=0.0,
+                    help="frontier arena per GPU (0 = 85%% of free HBM)")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    args = ap.parse_args()
+    if args.warmup < 3 and args.impl == "ours":
+        print("warning: the contract asks for >= 3 warm-up steps", file=sys.stderr)
+
+    build_fn, max_len, wdesc = WORKLOADS[args.workload]
+    g = build_fn()
+    if args.impl == "reference":
+        return run_reference(args, args.workload, g)
+
+    import torch
+    import torch.distributed as dist
+
+    from paper_1410_4876_b200 import binding
+
+    rank, world, local = dist_env()
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+    stream = torch.cuda.current_stream()
+    sh = stream.cuda_stream
+
+    free, _ = torch.cuda.mem_get_info()
+    l2_flush = torch.empty(512 << 20, dtype=torch.uint8, device=dev)  # > 126 MB L2
+    ws_bytes = int(args.workspace_gb * (1 << 30)) if args.workspace_gb > 0 else int(free * 0.85) - (1 << 30)
+    ws = torch.empty(ws_bytes, dtype=torch.uint8, device=dev)
+
+    opts = binding.make_options(device=local, stream=sh, max_len=max_len, shard_index=rank,
+                                shard_count=world, workspace=ws, profile=True)
+    graph = binding.cc_graph_from_csr(*g)  # resident for the device-timed steps
+
+    def step():
+        r = binding.cc_enumerate(graph, opts)
+        return r
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+
+    # ---- timed region: K steps, barrier + synchronize on both sides, events on the stream
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+    stats = []
+    results = []
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    with ClockSampler(local) as clk:
+        for i in range(args.steps):
+            l2_flush.zero_()  # flush L2 between timed iterations (outside the event window)
+            ev[i][0].record(stream)
+            r = step()
+            ev[i][1].record(stream)
+            results.append(r)
+        torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    dev_ms = sum(a.elapsed_time(b) for a, b in ev)
+    for r in results:
+        stats.append(binding.cc_result_stats(r))
+    counts, h = binding.cc_count_by_length(results[-1])
+    paths = binding.cc_paths_by_length(results[-1])
+
+    # ---- combine across ranks: counts + hash (SUM, the only data exchange) and time (MAX)
+    cyc_local = int(counts.sum())
+    paths_local = int(paths.sum())
+    if world > 1:
+        t = torch.tensor([dev_ms], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        dev_ms = float(t.item())
+        v = torch.tensor(np.concatenate([counts.astype(np.int64), [np.int64(np.uint64(h).view(np.int64))],
+                                         [paths_local]]), dtype=torch.int64, device=dev)
+        dist.all_reduce(v, op=dist.ReduceOp.SUM)
+        v = v.cpu().numpy()
+        counts = v[:-2].astype(np.uint64)
+        h = int(np.int64(v[-2]).view(np.uint64))
+        paths_total = int(v[-1])
+    else:
+        paths_total = paths_local
+    cycles_total = int(counts.sum())
+    ms_per_step = dev_ms / args.steps
+    value = cycles_total / (ms_per_step / 1e3)
+    paths_per_s = paths_total / (ms_per_step / 1e3)
+
+    # ---- roofline of the dominant kernel (Stage-2 expansion), from this rank's live events
+    st_last = stats[-1]
+    t_expand = sum(s["t_expand_ms"] for s in stats)
+    bytes_alg = sum(s["bytes_alg"] for s in stats)
+    launches = sum(s["launches"] for s in stats)
+    peak, peak_kind = peaks()
+    achieved = (bytes_alg / (t_expand / 1e3)) / 1e9 if t_expand > 0 else 0.0
+    traffic = None
+    tp = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    if os.path.exists(tp):
+        try:
+            traffic = json.load(open(tp)).get(args.workload)
+        except Exception:
+            traffic = None
+    roofline = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                "frac": achieved / peak, "traffic": traffic, "peak_kind": peak_kind,
+                "kernel": "k_expand_thread/k_expand_warp", "expand_share_of_step": t_expand / dev_ms if dev_ms else None,
+                "bytes_alg_per_step": bytes_alg / args.steps}
+
+    # ---- end to end through the public API with host buffers (labelling + upload + D2H)
+    e2e = None
+    if not args.no_e2e:
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+        h2d = d2h = 0
+        t0 = time.perf_counter()
+        ne = max(1, min(args.steps, 3))
+        for _ in range(ne):
+            gr = binding.cc_graph_from_csr(*g)  # host CSR -> labelling -> (upload in enumerate)
+            o2 = binding.make_options(device=local, stream=sh, max_len=max_len, shard_index=rank,
+                                      shard_count=world, workspace=ws)
+            r = binding.cc_enumerate(gr, o2)
+            c2, h2 = binding.cc_count_by_length(r)  # results on the host
+            s2 = binding.cc_result_stats(r)
+            h2d += s2["h2d_bytes"] + g[1].nbytes + g[2].nbytes
+            d2h += s2["d2h_bytes"]
+        torch.cuda.synchronize()
+        el = time.perf_counter() - t0
+        if world > 1:
+            t = torch.tensor([el], dtype=torch.float64, device=dev)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            el = float(t.item())
+        e2e = {"value": cycles_total / (el / ne), "unit": UNIT, "h2d_bytes_per_step": h2d // ne,
+               "d2h_bytes_per_step": d2h // ne, "ms_per_step": 1e3 * el / ne}
+
+    if rank == 0:
+        cpu = None
+        if not args.no_cpu_baseline and world == 1:
+            c, p, dt, cores, desc = oracle_sample(args.workload, g)
+            cpu = {"value": c / dt, "unit": UNIT, "cores": cores, "kind": "oracle", "sample": desc,
+                   "paths_per_s": p / dt, "seconds": dt}
+        line = {
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True,
+            "scaling": "strong", "vs_baseline": None, "dtype": "u64", "data": "synthetic",
+            "config": {"workload": args.workload, "description": wdesc, "n": g[0], "m": len(g[2]) // 2,
+                       "max_len": max_len, "l2": "flushed between steps (512 MB write)",
+                       "parallelism": f"shard{world}" if world > 1 else "single",
+                       "record_bytes": st_last["record_bytes"], "arena_records": st_last["arena_capacity"]},
+            "paths_per_s": paths_per_s, "cycles": cycles_total, "paths_expanded": paths_total,
+            "set_hash": f"{h:#018x}", "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e,
+            "gpu_launches": launches, "clocks": clk.summary(),
+            "frontier_sizes": {str(t): int(v) for t, v in enumerate(paths) if v} if world == 1 else None,
+            "per_step": {"chunks": st_last["chunks"], "rounds": st_last["rounds"],
+                         "peak_arena_records": st_last["peak_arena_records"],
+                         "t_stage1_ms": st_last["t_stage1_ms"], "t_expand_ms": st_last["t_expand_ms"]},
+        }
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+    return 0
+
+
+if __name__ == "__main__":
+    sys.exit(main())

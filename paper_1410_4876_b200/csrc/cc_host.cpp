@@ -1,0 +1,959 @@
+// cc_host.cpp -- C ABI (include/chordless.h) and the host orchestrator of the hot path.
+//
+//   cc_graph_from_csr   CSR validation/normalisation, degree labelling
+//                       (kept sequential on the host as the paper does),
+//                       relabelling so that internal id == label, forward-pair prefix sums for
+//                       Stage 1, adjacency bit rows (the bitmap form of PAPER.md:180 applied to
+//                       the graph itself).
+//   cc_enumerate        Alg. 4 HostProcess re-designed: instead of |V|-3
+//                       blind relaunches over one T/T' pair, a stack of frontier ranges in one
+//                       device arena.  Each step expands (a chunk of) the top level into the free
+//                       space above it; whole levels are expanded at once while they fit, so the
+//                       common case is plain level-synchronous BFS, and it degrades to
+//                       depth-first over chunks when the next frontier would exceed the arena
+//                       (the RAM<->GPU "data transportation" future work of PAPER.md:455).
+//                       Early exit when a level is empty (reading G9).
+#include "../../include/chordless.h"
+#include "cc_internal.h"
+
+#include <algorithm>
+#include <chrono>
+#include <cstddef>
+#include <cstdio>
+#include <cstdlib>
+#include <cstring>
+#include <memory>
+#include <mutex>
+#include <set>
+#include <string>
+#include <vector>
+
+using cc::u64;
+
+namespace {
+
+thread_local std::string g_last_error;
+
+cc_status fail(cc_status s, const std::string &msg)
+{
+    g_last_error = msg;
+    return s;
+}
+
+cc_status cuda_fail(cudaError_t e, const char *where)
+{
+    return fail(CC_ERR_CUDA, std::string(where) + ": " + cudaGetErrorString(e));
+}
+
+#define CC_CUDA(call)                                   \
+    do {                                                \
+        cudaError_t e__ = (call);                       \
+        if (e__ != cudaSuccess)                         \
+            return cuda_fail(e__, #call);               \
+    } while (0)
+
+double now_ms()
+{
+    return std::chrono::duration<double, std::milli>(
+               std::chrono::steady_clock::now().time_since_epoch())
+        .count();
+}
+
+}  // namespace
+
+// ------------------------------------------------------------------------------ graph
+struct DevCopy {
+    int device = -1;
+    void *buf = nullptr;       // rowptr | col | fwd | pair_prefix | adj | orig | key
+    size_t bytes = 0;
+    u64 key_seed = 0;
+    bool keys_valid = false;
+    cc::DevGraph dg{};
+};
+
+struct cc_graph {
+    int64_t n = 0, m = 0, max_deg = 0;
+    std::vector<int32_t> label;     // original id -> label
+    std::vector<int32_t> perm;      // label -> original id
+    std::vector<uint32_t> irow;     // relabelled CSR (internal id == label)
+    std::vector<uint32_t> icol;
+    std::vector<uint32_t> ifwd;
+    std::vector<u64> pair_prefix;
+    int nw = 0;                     // 0 = outside the bitmap size class
+    std::vector<u64> adj;
+    double t_build_ms = 0;
+    std::mutex mu;
+    std::vector<DevCopy> dev;
+};
+
+extern "C" void cc_options_init(cc_options *o)
+{
+    if (!o)
+        return;
+    std::memset(o, 0, sizeof(*o));
+    o->struct_size = sizeof(cc_options);
+    o->device = -1;
+    o->shard_count = 1;
+}
+
+extern "C" const char *cc_last_error(void) { return g_last_error.c_str(); }
+
+extern "C" const char *cc_status_string(cc_status s)
+{
+    switch (s) {
+    case CC_OK: return "CC_OK";
+    case CC_ERR_INVALID_ARGUMENT: return "CC_ERR_INVALID_ARGUMENT";
+    case CC_ERR_INVALID_VERTEX: return "CC_ERR_INVALID_VERTEX";
+    case CC_ERR_SELF_LOOP: return "CC_ERR_SELF_LOOP";
+    case CC_ERR_NOT_SYMMETRIC: return "CC_ERR_NOT_SYMMETRIC";
+    case CC_ERR_CAPACITY: return "CC_ERR_CAPACITY";
+    case CC_ERR_CUDA: return "CC_ERR_CUDA";
+    case CC_ERR_NOT_COLLECTED: return "CC_ERR_NOT_COLLECTED";
+    case CC_ERR_BUFFER_TOO_SMALL: return "CC_ERR_BUFFER_TOO_SMALL";
+    case CC_ERR_TOO_LARGE: return "CC_ERR_TOO_LARGE";
+    case CC_ERR_NO_DEVICE: return "CC_ERR_NO_DEVICE";
+    }
+    return "CC_ERR_UNKNOWN";
+}
+
+extern "C" const char *cc_version(void) { return "chordless-b200 0.1 (sm_100a)"; }
+
+// Degree labelling: repeatedly delete a vertex of minimum degree in the
+// remaining graph, l(u_i) = i; ties to the lowest original id.  Ordered set keyed
+// (degree, id), O((n + m) log n).
+static void degree_labeling(int64_t n, const std::vector<int64_t> &rp, const std::vector<int32_t> &cl,
+                            std::vector<int32_t> &label)
+{
+    std::vector<int64_t> d(n);
+    std::set<std::pair<int64_t, int32_t>> q;
+    for (int64_t v = 0; v < n; ++v) {
+        d[v] = rp[v + 1] - rp[v];
+        q.insert({d[v], (int32_t)v});
+    }
+    label.assign(n, -1);
+    for (int64_t i = 0; i < n; ++i) {
+        auto it = q.begin();
+        const int32_t u = it->second;
+        q.erase(it);
+        label[u] = (int32_t)i;
+        for (int64_t k = rp[u]; k < rp[u + 1]; ++k) {
+            const int32_t w = cl[k];
+            if (label[w] < 0) {
+                q.erase({d[w], w});
+                --d[w];
+                q.insert({d[w], w});
+            }
+        }
+    }
+}
+
+extern "C" cc_status cc_graph_from_csr(int64_t n, const int64_t *row_ptr, const int32_t *col_idx,
+                                       cc_graph **out)
+{
+    if (!out)
+        return fail(CC_ERR_INVALID_ARGUMENT, "out is NULL");
+    if (n < 0 || n > (1 << 20))
+        return fail(CC_ERR_INVALID_ARGUMENT, "n must be in [0, 2^20]");
+    if (n > 0 && !row_ptr)
+        return fail(CC_ERR_INVALID_ARGUMENT, "row_ptr is NULL");
+    const double t0 = now_ms();
+    if (n > 0) {
+        if (row_ptr[0] != 0)
+            return fail(CC_ERR_INVALID_ARGUMENT, "row_ptr[0] != 0");
+        for (int64_t v = 0; v < n; ++v)
+            if (row_ptr[v + 1] < row_ptr[v])
+                return fail(CC_ERR_INVALID_ARGUMENT, "row_ptr is decreasing");
+        if (row_ptr[n] > 0 && !col_idx)
+            return fail(CC_ERR_INVALID_ARGUMENT, "col_idx is NULL");
+        if (row_ptr[n] > (int64_t)1 << 31)
+            return fail(CC_ERR_INVALID_ARGUMENT, "more than 2^31 adjacency entries");
+    }
+    // normalise: sort + dedup each row, validate ids and self-loops
+    std::vector<int64_t> rp(n + 1, 0);
+    std::vector<int32_t> cl;
+    cl.reserve(n > 0 ? (size_t)row_ptr[n] : 0);
+    for (int64_t v = 0; v < n; ++v) {
+        const size_t b = cl.size();
+        for (int64_t k = row_ptr[v]; k < row_ptr[v + 1]; ++k) {
+            const int32_t w = col_idx[k];
+            if (w < 0 || w >= n)
+                return fail(CC_ERR_INVALID_VERTEX, "vertex id " + std::to_string(w) + " in row " +
+                                                       std::to_string(v) + " outside [0, n)");
+            if (w == v)
+                return fail(CC_ERR_SELF_LOOP, "self-loop at vertex " + std::to_string(v));
+            cl.push_back(w);
+        }
+        std::sort(cl.begin() + b, cl.end());
+        cl.erase(std::unique(cl.begin() + b, cl.end()), cl.end());
+        rp[v + 1] = (int64_t)cl.size();
+    }
+    // symmetry: w in row v  <=>  v in row w
+    for (int64_t v = 0; v < n; ++v)
+        for (int64_t k = rp[v]; k < rp[v + 1]; ++k) {
+            const int32_t w = cl[k];
+            if (!std::binary_search(cl.begin() + rp[w], cl.begin() + rp[w + 1], (int32_t)v))
+                return fail(CC_ERR_NOT_SYMMETRIC, "edge (" + std::to_string(v) + "," +
+                                                      std::to_string(w) + ") has no reverse entry");
+        }
+
+    cc_graph *g = new cc_graph();
+    g->n = n;
+    g->m = (int64_t)cl.size() / 2;
+    for (int64_t v = 0; v < n; ++v)
+        g->max_deg = std::max<int64_t>(g->max_deg, rp[v + 1] - rp[v]);
+    degree_labeling(n, rp, cl, g->label);
+    g->perm.assign(n, 0);
+    for (int64_t v = 0; v < n; ++v)
+        g->perm[g->label[v]] = (int32_t)v;
+    // relabelled CSR: row of internal vertex i = labels of the neighbours of perm[i], sorted
+    g->irow.assign(n + 1, 0);
+    g->icol.resize(cl.size());
+    g->ifwd.assign(n, 0);
+    g->pair_prefix.assign(n + 1, 0);
+    for (int64_t i = 0; i < n; ++i) {
+        const int32_t v = g->perm[i];
+        const uint32_t b = g->irow[i];
+        uint32_t k = b;
+        for (int64_t e = rp[v]; e < rp[v + 1]; ++e)
+            g->icol[k++] = (uint32_t)g->label[cl[e]];
+        std::sort(g->icol.begin() + b, g->icol.begin() + k);
+        g->irow[i + 1] = k;
+        uint32_t f = b;
+        while (f < k && g->icol[f] <= (uint32_t)i)
+            ++f;
+        g->ifwd[i] = f;
+        const u64 dplus = k - f;
+        g->pair_prefix[i + 1] = g->pair_prefix[i] + dplus * (dplus - 1) / 2;
+    }
+    if (n <= 64 * cc::kMaxWords) {
+        g->nw = n > 0 ? (int)((n + 63) / 64) : 1;
+        g->adj.assign((size_t)n * g->nw, 0);
+        for (int64_t i = 0; i < n; ++i)
+            for (uint32_t k = g->irow[i]; k < g->irow[i + 1]; ++k) {
+                const uint32_t w = g->icol[k];
+                g->adj[(size_t)i * g->nw + (w >> 6)] |= 1ull << (w & 63);
+            }
+    }
+    g->t_build_ms = now_ms() - t0;
+    *out = g;
+    return CC_OK;
+}
+
+extern "C" void cc_graph_free(cc_graph *g)
+{
+    if (!g)
+        return;
+    int cur = -1;
+    cudaGetDevice(&cur);
+    for (auto &d : g->dev)
+        if (d.buf) {
+            cudaSetDevice(d.device);
+            cudaFree(d.buf);
+        }
+    if (cur >= 0)
+        cudaSetDevice(cur);
+    delete g;
+}
+
+extern "C" cc_status cc_graph_info(const cc_graph *g, int64_t *n, int64_t *m, int64_t *max_degree)
+{
+    if (!g)
+        return fail(CC_ERR_INVALID_ARGUMENT, "graph is NULL");
+    if (n)
+        *n = g->n;
+    if (m)
+        *m = g->m;
+    if (max_degree)
+        *max_degree = g->max_deg;
+    return CC_OK;
+}
+
+extern "C" cc_status cc_graph_labels(const cc_graph *g, int32_t *labels)
+{
+    if (!g || (!labels && g->n > 0))
+        return fail(CC_ERR_INVALID_ARGUMENT, "NULL argument");
+    std::copy(g->label.begin(), g->label.end(), labels);
+    return CC_OK;
+}
+
+static size_t align_up(size_t x, size_t a) { return (x + a - 1) / a * a; }
+
+// Upload (once per device) the relabelled graph; recompute keys when the seed changes.
+static cc_status ensure_device_graph(cc_graph *g, int device, u64 seed, cudaStream_t st, DevCopy **out,
+                                     uint64_t *h2d)
+{
+    DevCopy *dc = nullptr;
+    for (auto &d : g->dev)
+        if (d.device == device)
+            dc = &d;
+    const int64_t n = g->n;
+    if (!dc) {
+        g->dev.emplace_back();
+        dc = &g->dev.back();
+        dc->device = device;
+        const size_t s_row = align_up((n + 1) * 4, 256), s_col = align_up(std::max<size_t>(g->icol.size(), 1) * 4, 256),
+                     s_fwd = align_up(std::max<int64_t>(n, 1) * 4, 256), s_pp = align_up((n + 1) * 8, 256),
+                     s_adj = align_up(std::max<size_t>(g->adj.size(), 1) * 8, 256),
+                     s_orig = align_up(std::max<int64_t>(n, 1) * 4, 256), s_key = align_up(std::max<int64_t>(n, 1) * 8, 256),
+                     s_kb = g->nw <= cc::kByteTableWords ? align_up((size_t)8 * g->nw * 256 * 8, 256) : 256;
+        dc->bytes = s_row + s_col + s_fwd + s_pp + s_adj + s_orig + s_key + s_kb;
+        CC_CUDA(cudaMalloc(&dc->buf, dc->bytes));
+        char *p = (char *)dc->buf;
+        auto *rowptr = (uint32_t *)p; p += s_row;
+        auto *col = (uint32_t *)p; p += s_col;
+        auto *fwd = (uint32_t *)p; p += s_fwd;
+        auto *pp = (u64 *)p; p += s_pp;
+        auto *adj = (u64 *)p; p += s_adj;
+        auto *orig = (int32_t *)p; p += s_orig;
+        auto *key = (u64 *)p; p += s_key;
+        auto *keybyte = (u64 *)p;
+        CC_CUDA(cudaMemcpyAsync(rowptr, g->irow.data(), (n + 1) * 4, cudaMemcpyHostToDevice, st));
+        if (!g->icol.empty())
+            CC_CUDA(cudaMemcpyAsync(col, g->icol.data(), g->icol.size() * 4, cudaMemcpyHostToDevice, st));
+        if (n > 0) {
+            CC_CUDA(cudaMemcpyAsync(fwd, g->ifwd.data(), n * 4, cudaMemcpyHostToDevice, st));
+            CC_CUDA(cudaMemcpyAsync(orig, g->perm.data(), n * 4, cudaMemcpyHostToDevice, st));
+        }
+        CC_CUDA(cudaMemcpyAsync(pp, g->pair_prefix.data(), (n + 1) * 8, cudaMemcpyHostToDevice, st));
+        if (!g->adj.empty())
+            CC_CUDA(cudaMemcpyAsync(adj, g->adj.data(), g->adj.size() * 8, cudaMemcpyHostToDevice, st));
+        *h2d += (n + 1) * 4 + g->icol.size() * 4 + n * 8 + (n + 1) * 8 + g->adj.size() * 8;
+        dc->dg.n = (int32_t)n;
+        dc->dg.nw = g->nw;
+        dc->dg.rowptr = rowptr;
+        dc->dg.col = col;
+        dc->dg.fwd = fwd;
+        dc->dg.pair_prefix = pp;
+        dc->dg.adj = adj;
+        dc->dg.key = key;
+        dc->dg.keybyte = keybyte;
+        dc->dg.orig = orig;
+    }
+    if (!dc->keys_valid || dc->key_seed != seed) {
+        CC_CUDA(cc::launch_keys((u64 *)dc->dg.key, (u64 *)dc->dg.keybyte, dc->dg.orig, (int)n, g->nw, seed, st));
+        dc->key_seed = seed;
+        dc->keys_valid = true;
+    }
+    *out = dc;
+    return CC_OK;
+}
+
+// ------------------------------------------------------------------------------ result
+struct cc_result {
+    int64_t n = 0;
+    std::vector<u64> counts, paths, cand;
+    u64 hash = 0;
+    cc_stats stats{};
+    bool collected = false;
+    int device = -1;
+    int nw = 1;
+    void *cyc_buf = nullptr;     // CycleStore s | ids, then adj copy, orig copy
+    cc::CycleStore cyc{};
+    u64 *adj = nullptr;
+    int32_t *orig = nullptr;
+    u64 n_cyc = 0;
+};
+
+extern "C" void cc_result_free(cc_result *r)
+{
+    if (!r)
+        return;
+    if (r->cyc_buf) {
+        int cur = -1;
+        cudaGetDevice(&cur);
+        cudaSetDevice(r->device);
+        cudaFree(r->cyc_buf);
+        if (cur >= 0)
+            cudaSetDevice(cur);
+    }
+    delete r;
+}
+namespace {
+
+// Scoped device allocation on a stream (stream-ordered allocator).
+struct DevBuf {
+    void *p = nullptr;
+    cudaStream_t st = nullptr;
+    ~DevBuf()
+    {
+        if (p)
+            cudaFreeAsync(p, st);
+    }
+};
+
+// Per-thread pinned host staging (scratch read-back, page tables).
+struct Pinned {
+    void *p = nullptr;
+    size_t bytes = 0;
+    ~Pinned()
+    {
+        if (p)
+            cudaFreeHost(p);
+    }
+    cudaError_t reserve(size_t b)
+    {
+        if (b <= bytes)
+            return cudaSuccess;
+        if (p)
+            cudaFreeHost(p);
+        p = nullptr;
+        bytes = 0;
+        cudaError_t e = cudaMallocHost(&p, b);
+        if (e == cudaSuccess)
+            bytes = b;
+        return e;
+    }
+};
+thread_local Pinned t_pinned;
+
+void set_pool_threshold(int device)
+{
+    static std::mutex mu;
+    static std::vector<int> done;
+    std::lock_guard<std::mutex> lk(mu);
+    if (std::find(done.begin(), done.end(), device) != done.end())
+        return;
+    cudaMemPool_t pool;
+    if (cudaDeviceGetDefaultMemPool(&pool, device) == cudaSuccess) {
+        u64 thr = ~0ull;
+        cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+    }
+    done.push_back(device);
+}
+
+// One frontier level F_t: a list of arena pages, all full except the last.
+struct Level {
+    std::vector<uint32_t> pages;
+    u64 count = 0;
+    bool sharded = false;   // paths already partitioned between shards (owned by this one)
+    bool init = false;      // sharded flag fixed (at the level's first write)
+    double fan = 0;         // observed extensions per path at this level (0 = unknown)
+};
+
+}  // namespace
+
+static cc_status enumerate_impl(const cc_graph *cg, const cc_options *opt_in, cc_result **out,
+                                u64 *need_cycles)
+{
+    const double t_wall0 = now_ms();
+    if (!cg || !out)
+        return fail(CC_ERR_INVALID_ARGUMENT, "NULL argument");
+    cc_options opt;
+    cc_options_init(&opt);
+    if (opt_in) {
+        if (opt_in->struct_size < sizeof(uint32_t) || opt_in->struct_size > sizeof(cc_options))
+            return fail(CC_ERR_INVALID_ARGUMENT, "cc_options.struct_size mismatch");
+        std::memcpy(&opt, opt_in, opt_in->struct_size);
+    }
+    if (opt.shard_count < 1 || opt.shard_index >= opt.shard_count)
+        return fail(CC_ERR_INVALID_ARGUMENT, "need 0 <= shard_index < shard_count");
+    if (opt.root_stride > 1 && opt.root_offset >= opt.root_stride)
+        return fail(CC_ERR_INVALID_ARGUMENT, "need root_offset < root_stride");
+    cc_graph *g = const_cast<cc_graph *>(cg);
+    const int64_t n = g->n;
+    if (n > 0 && g->nw == 0)
+        return fail(CC_ERR_TOO_LARGE, "n = " + std::to_string(n) + " exceeds the bitmap size class (n <= " +
+                                          std::to_string(64 * cc::kMaxWords) + ")");
+    int ndev = 0;
+    if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0)
+        return fail(CC_ERR_NO_DEVICE, "no CUDA device");
+    int device = opt.device;
+    if (device < 0)
+        CC_CUDA(cudaGetDevice(&device));
+    if (device >= ndev)
+        return fail(CC_ERR_NO_DEVICE, "device ordinal out of range");
+    CC_CUDA(cudaSetDevice(device));
+    cudaStream_t st = (cudaStream_t)opt.stream;
+    const u64 seed = opt.hash_seed ? opt.hash_seed : 0x1410487600000000ULL;
+
+    std::lock_guard<std::mutex> lk(g->mu);
+    cc_result *res = new cc_result();
+    std::unique_ptr<cc_result, void (*)(cc_result *)> res_guard(res, cc_result_free);
+    res->n = n;
+    res->counts.assign(n + 2, 0);
+    res->paths.assign(n + 2, 0);
+    res->cand.assign(n + 2, 0);
+    res->device = device;
+    res->nw = std::max(g->nw, 1);
+    res->collected = opt.collect != 0;
+    cc_stats &S = res->stats;
+    S.struct_size = sizeof(cc_stats);
+    S.n_words = res->nw;
+    S.t_labeling_ms = g->t_build_ms;
+
+    if (n < 3) {  // no cycle possible
+        S.t_wall_ms = now_ms() - t_wall0;
+        *out = res_guard.release();
+        return CC_OK;
+    }
+    int sms = 0;
+    CC_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device));
+    set_pool_threshold(device);
+
+    DevCopy *dc = nullptr;
+    {
+        cc_status s = ensure_device_graph(g, device, seed, st, &dc, &S.h2d_bytes);
+        if (s != CC_OK)
+            return s;
+    }
+    const int nw = g->nw;
+    const u64 rec_bytes = (u64)nw * 8 + 4;
+    S.record_bytes = rec_bytes;
+
+    // ---- frontier arena, split into pages of P = 2^lp records
+    DevBuf ws_own;
+    ws_own.st = st;
+    void *ws = opt.workspace;
+    u64 ws_bytes = opt.workspace_bytes;
+    if (!ws) {
+        if (ws_bytes == 0) {
+            size_t fr = 0, tot = 0;
+            CC_CUDA(cudaMemGetInfo(&fr, &tot));
+            ws_bytes = std::max<u64>(fr / 4, 64ull << 20);
+        }
+        CC_CUDA(cudaMallocAsync(&ws_own.p, ws_bytes, st));
+        ws = ws_own.p;
+    }
+    uint32_t lp = 20;  // 1 Mi records per page, fewer if the arena would have < 64 pages
+    while (lp > (uint32_t)cc::kMinLogPage && (ws_bytes / (((u64)1 << lp) * rec_bytes)) < 64)
+        --lp;
+    const u64 P = (u64)1 << lp;
+    const u64 page_bytes = P * rec_bytes;
+    const u64 npages = ws_bytes / page_bytes;
+    if (npages < 2)
+        return fail(CC_ERR_CAPACITY, "workspace of " + std::to_string(ws_bytes) + " B holds fewer than 2 pages of " +
+                                         std::to_string(P) + " records");
+    S.arena_capacity = npages * P;
+    std::vector<uint32_t> free_pages;
+    free_pages.reserve(npages);
+    for (u64 i = npages; i-- > 0;)
+        free_pages.push_back((uint32_t)i);
+
+    // ---- control block: Scratch | page table (in pages, then out pages)
+    DevBuf ctrl;
+    ctrl.st = st;
+    const size_t ctrl_bytes = sizeof(cc::Scratch) + (size_t)2 * npages * 4 + 256;
+    CC_CUDA(cudaMallocAsync(&ctrl.p, ctrl_bytes, st));
+    CC_CUDA(cudaMemsetAsync(ctrl.p, 0, sizeof(cc::Scratch), st));
+    cc::Scratch *d_sc = (cc::Scratch *)ctrl.p;
+    uint32_t *d_tab = (uint32_t *)((char *)ctrl.p + sizeof(cc::Scratch));
+    CC_CUDA(t_pinned.reserve(sizeof(cc::Scratch) + (size_t)2 * npages * 4 + 64));
+    cc::Scratch *h_sc = (cc::Scratch *)t_pinned.p;
+    uint32_t *h_tab = (uint32_t *)((char *)t_pinned.p + sizeof(cc::Scratch));
+
+    // ---- collect store
+    if (opt.collect) {
+        const u64 ccap = opt.collect_capacity ? opt.collect_capacity : (1ull << 22);
+        const size_t s_s = align_up(ccap * nw * 8, 256), s_ids = align_up(ccap * 4, 256),
+                     s_adj = align_up((size_t)n * nw * 8, 256), s_orig = align_up((size_t)n * 4, 256);
+        CC_CUDA(cudaMalloc(&res->cyc_buf, s_s + s_ids + s_adj + s_orig));
+        char *p = (char *)res->cyc_buf;
+        res->cyc.s = (u64 *)p;
+        res->cyc.ids = (uint32_t *)(p + s_s);
+        res->cyc.cap = ccap;
+        res->cyc.count = &d_sc->cyc_count;
+        res->adj = (u64 *)(p + s_s + s_ids);
+        res->orig = (int32_t *)(p + s_s + s_ids + s_adj);
+        CC_CUDA(cudaMemcpyAsync(res->adj, dc->dg.adj, (size_t)n * nw * 8, cudaMemcpyDeviceToDevice, st));
+        CC_CUDA(cudaMemcpyAsync(res->orig, dc->dg.orig, (size_t)n * 4, cudaMemcpyDeviceToDevice, st));
+    }
+
+    cc::LaunchArgs base{};
+    base.g = dc->dg;
+    base.pg.base = (char *)ws;
+    base.pg.page_bytes = page_bytes;
+    base.pg.log_p = lp;
+    base.pg.in_pages = d_tab;
+    base.pg.out_pages = d_tab + npages;
+    base.cyc = res->cyc;
+    base.sc = d_sc;
+    base.collect = opt.collect ? 1 : 0;
+    base.root_stride = opt.root_stride;
+    base.root_offset = opt.root_offset;
+    base.shard_index = opt.shard_index;
+    base.shard_count = opt.shard_count;
+
+    const cc::ExpandVariant variant = g->max_deg <= 32 ? cc::ExpandVariant::Thread : cc::ExpandVariant::Warp;
+    const size_t gsmem = ((size_t)n * (nw + 1) + (nw <= cc::kByteTableWords ? (size_t)8 * nw * 256 : 0)) * 8;
+    const int grid_s1 = cc::max_blocks_per_sm(0, nw, gsmem) * sms;
+    const int grid_ex = cc::max_blocks_per_sm(variant == cc::ExpandVariant::Thread ? 1 : 2, nw, gsmem) * sms;
+    const int grid_sf = cc::max_blocks_per_sm(3, nw, 0) * sms;
+    const double maxfan = (double)std::max<int64_t>(g->max_deg - 1, 1);
+    const uint32_t W = opt.shard_count;
+    const u64 shard_threshold = (u64)(opt.min_shard_paths ? opt.min_shard_paths : 1024) * W;
+    const uint32_t max_len = opt.max_len;
+    const bool want_paths = max_len == 0 || max_len >= 4;
+
+    cudaEvent_t ev0, ev1, ea, eb;
+    CC_CUDA(cudaEventCreate(&ev0));
+    CC_CUDA(cudaEventCreate(&ev1));
+    CC_CUDA(cudaEventCreate(&ea));
+    CC_CUDA(cudaEventCreate(&eb));
+    struct EvGuard {
+        cudaEvent_t e[4];
+        ~EvGuard()
+        {
+            for (auto x : e)
+                cudaEventDestroy(x);
+        }
+    } evg{{ev0, ev1, ea, eb}};
+    CC_CUDA(cudaEventRecord(ev0, st));
+
+    u64 cyc_committed = 0;   // collect-store counter after the last committed launch
+    u64 in_use = 0, high_water = 0;
+
+    // Launch one kernel over the page list `in` (or a Stage-1 pair range) writing into the
+    // free pages; on success the used output pages are returned in `used` and the scratch
+    // in *h_sc.  Returns CC_OK, or CC_ERR_CAPACITY with *overflow set when the output did not
+    // fit (nothing is committed: the caller retries with less input).
+    enum Kind { STAGE1, EXPAND, FILTER };
+    auto launch = [&](Kind kind, const uint32_t *in, size_t n_in_pages, u64 n_in, u64 pair_lo, bool emit,
+                      bool count, bool filter, std::vector<uint32_t> &used, bool *overflow) -> cc_status {
+        *overflow = false;
+        const size_t nfree = free_pages.size();
+        // page table: input pages, then every free page (in pop order) as potential output
+        for (size_t i = 0; i < n_in_pages; ++i)
+            h_tab[i] = in[i];
+        for (size_t i = 0; i < nfree; ++i)
+            h_tab[npages + i] = free_pages[nfree - 1 - i];
+        if (n_in_pages)
+            CC_CUDA(cudaMemcpyAsync(d_tab, h_tab, n_in_pages * 4, cudaMemcpyHostToDevice, st));
+        if (emit && nfree)
+            CC_CUDA(cudaMemcpyAsync(d_tab + npages, h_tab + npages, nfree * 4, cudaMemcpyHostToDevice, st));
+        S.h2d_bytes += (n_in_pages + (emit ? nfree : 0)) * 4;
+        CC_CUDA(cudaMemsetAsync(d_sc, 0, offsetof(cc::Scratch, cyc_count), st));
+        cc::LaunchArgs a = base;
+        a.in_lo = pair_lo;
+        a.n_in = n_in;
+        a.out_off = 0;
+        a.out_cap = emit ? nfree * P : 0;
+        a.emit = emit ? 1 : 0;
+        a.count = count ? 1 : 0;
+        a.filter = filter ? 1 : 0;
+        if (opt.profile)
+            CC_CUDA(cudaEventRecord(ea, st));
+        if (kind == STAGE1)
+            CC_CUDA(cc::launch_stage1(a, st, grid_s1));
+        else if (kind == EXPAND)
+            CC_CUDA(cc::launch_expand(a, variant, st, grid_ex));
+        else
+            CC_CUDA(cc::launch_shard_filter(a, st, grid_sf));
+        if (opt.profile)
+            CC_CUDA(cudaEventRecord(eb, st));
+        CC_CUDA(cudaMemcpyAsync(h_sc, d_sc, sizeof(cc::Scratch), cudaMemcpyDeviceToHost, st));
+        CC_CUDA(cudaStreamSynchronize(st));
+        S.d2h_bytes += sizeof(cc::Scratch);
+        S.launches++;
+        if (opt.profile) {
+            float ms = 0;
+            CC_CUDA(cudaEventElapsedTime(&ms, ea, eb));
+            if (kind == STAGE1)
+                S.t_stage1_ms += ms;
+            else if (kind == EXPAND)
+                S.t_expand_ms += ms;
+        }
+        if (h_sc->err || h_sc->out_count > a.out_cap) {
+            *overflow = true;
+            if (opt.collect) {  // roll back the cycles this launch stored
+                CC_CUDA(cudaMemcpyAsync(&d_sc->cyc_count, &cyc_committed, 8, cudaMemcpyHostToDevice, st));
+                CC_CUDA(cudaStreamSynchronize(st));
+            }
+            return CC_OK;
+        }
+        cyc_committed = h_sc->cyc_count;
+        const u64 npg = (h_sc->out_count + P - 1) / P;
+        used.clear();
+        for (u64 i = 0; i < npg; ++i) {
+            used.push_back(free_pages.back());
+            free_pages.pop_back();
+        }
+        return CC_OK;
+    };
+
+    std::vector<Level> levels(n + 3);
+    const bool count_tri = opt.shard_index == 0 && (opt.root_stride <= 1 || opt.root_offset == 0);
+    const u64 stage1_total = g->pair_prefix[n];
+    S.stage1_pairs = stage1_total;
+    u64 s1_next = 0;
+    // shard at Stage 1 when the seed space alone is large enough (deterministic: graph-only)
+    const bool s1_filter = W > 1 && stage1_total >= shard_threshold;
+    levels[3].init = true;
+    levels[3].sharded = W == 1 || s1_filter;
+    int deepest = 2;  // levels 3..deepest may be non-empty
+    std::vector<uint32_t> used;
+
+    while (true) {
+        while (deepest >= 3 && levels[deepest].count == 0)
+            --deepest;
+        if (deepest < 3) {
+            // ---- Stage 1 (Alg. 2): the next chunk of forward pairs -> F_3 and triangles
+            if (s1_next >= stage1_total)
+                break;
+            const u64 c = std::min<u64>(stage1_total - s1_next, (u64)free_pages.size() * P);
+            if (c == 0)
+                return fail(CC_ERR_CAPACITY, "no free arena page for Stage 1");
+            bool of = false;
+            cc_status s = launch(STAGE1, nullptr, 0, c, s1_next, want_paths, count_tri, s1_filter, used, &of);
+            if (s != CC_OK)
+                return s;
+            if (of)
+                return fail(CC_ERR_CAPACITY, "Stage 1 output overflow (internal sizing error)");
+            s1_next += c;
+            S.chunks++;
+            res->counts[3] += h_sc->cycles;
+            res->hash += h_sc->hash;
+            Level &L3 = levels[3];
+            L3.pages = used;
+            L3.count = h_sc->out_count;
+            in_use += L3.count;
+            high_water = std::max(high_water, in_use);
+            deepest = 3;
+            continue;
+        }
+        const int d = deepest;
+        Level &L = levels[d];
+        // ---- multi-GPU: partition the first frontier level with >= threshold paths
+        if (W > 1 && !L.sharded && L.count >= shard_threshold) {
+            bool of = false;
+            cc_status s = launch(FILTER, L.pages.data(), L.pages.size(), L.count, 0, true, false, false, used, &of);
+            if (s != CC_OK)
+                return s;
+            if (of)
+                return fail(CC_ERR_CAPACITY, "workspace too small for the shard filter");
+            for (uint32_t pg : L.pages)
+                free_pages.push_back(pg);
+            in_use -= L.count;
+            L.pages = used;
+            L.count = h_sc->out_count;
+            in_use += L.count;
+            L.sharded = true;
+            continue;
+        }
+        const bool owner = W == 1 || L.sharded || opt.shard_index == 0;
+        const bool emit = max_len == 0 || (u64)d + 1 < max_len;
+        Level &C = levels[d + 1];
+        if (emit && !C.init) {
+            C.init = true;
+            C.sharded = L.sharded;
+        }
+        // ---- choose the input chunk: the last k pages of F_d
+        size_t k = L.pages.size();
+        if (emit && (W == 1 || L.sharded)) {
+            double f = L.fan > 0 ? L.fan * 1.15 : (levels[d - 1].fan > 0 ? levels[d - 1].fan * 1.5 : maxfan);
+            f = std::min(std::max(f, 0.05), maxfan);
+            const double room = (double)free_pages.size() * P;
+            // records of the last k pages: (k-1) full pages + the partial last page
+            const u64 last_fill = L.count - (u64)(L.pages.size() - 1) * P;
+            u64 take = (u64)std::max(1.0, room / f);
+            if (take >= L.count)
+                k = L.pages.size();
+            else if (take <= last_fill)
+                k = 1;
+            else
+                k = 1 + (size_t)((take - last_fill) / P);
+        }
+        for (;;) {
+            const u64 last_fill = L.count - (u64)(L.pages.size() - 1) * P;
+            const u64 c = last_fill + (u64)(k - 1) * P;
+            const uint32_t *in = L.pages.data() + (L.pages.size() - k);
+            bool of = false;
+            cc_status s = launch(EXPAND, in, k, c, 0, emit, owner, false, used, &of);
+            if (s != CC_OK)
+                return s;
+            if (of) {
+                if (W > 1 && !L.sharded)
+                    return fail(CC_ERR_CAPACITY, "workspace too small to expand the unsharded level F_" +
+                                                     std::to_string(d) + " whole (needed before sharding)");
+                if (k == 1)
+                    return fail(CC_ERR_CAPACITY, "workspace too small: one page of F_" + std::to_string(d) +
+                                                     " needs " + std::to_string(h_sc->out_count) +
+                                                     " output records, " + std::to_string(free_pages.size() * P) +
+                                                     " free");
+                L.fan = std::max(L.fan, (double)h_sc->out_count / (double)c);
+                const double room = (double)free_pages.size() * P;
+                const double want = room / (L.fan * 1.15);
+                size_t k2 = want <= last_fill ? 1 : 1 + (size_t)((want - last_fill) / P);
+                k = std::max<size_t>(1, std::min(k2, k - 1));
+                continue;
+            }
+            // commit
+            S.chunks++;
+            S.rounds = std::max<u64>(S.rounds, (u64)d);
+            if (owner) {
+                res->paths[d] += c;
+                res->cand[d] += h_sc->cand;
+                S.paths_expanded += c;
+                res->counts[d + 1] += h_sc->cycles;
+                res->hash += h_sc->hash;
+            }
+            S.bytes_alg += (c + h_sc->out_count) * rec_bytes;
+            if (c > 0)
+                L.fan = (double)h_sc->out_count / (double)c;
+            for (size_t i = 0; i < k; ++i) {
+                free_pages.push_back(L.pages.back());
+                L.pages.pop_back();
+            }
+            L.count -= c;
+            in_use -= c;
+            if (h_sc->out_count) {
+                C.pages = used;
+                C.count = h_sc->out_count;
+                in_use += C.count;
+                high_water = std::max(high_water, in_use);
+                deepest = d + 1;
+            }
+            break;
+        }
+    }
+    S.peak_arena_records = high_water;
+
+    CC_CUDA(cudaEventRecord(ev1, st));
+    CC_CUDA(cudaStreamSynchronize(st));
+    float tdev = 0;
+    CC_CUDA(cudaEventElapsedTime(&tdev, ev0, ev1));
+    S.t_dev_ms = tdev;
+    for (int64_t k = 0; k <= n; ++k) {
+        S.total_cycles += res->counts[k];
+        S.candidates += res->cand[k];
+    }
+    S.triplets = res->paths[3];
+    const u64 ncyc = cyc_committed;
+    S.cycles_stored = ncyc;
+    if (opt.collect) {
+        S.bytes_alg += std::min<u64>(ncyc, res->cyc.cap) * rec_bytes;
+        if (ncyc > res->cyc.cap) {
+            *need_cycles = ncyc;
+            return fail(CC_ERR_CAPACITY, "collect capacity " + std::to_string(res->cyc.cap) +
+                                             " exceeded: " + std::to_string(ncyc) + " cycles");
+        }
+        res->n_cyc = ncyc;
+    }
+    S.t_wall_ms = now_ms() - t_wall0;
+    *out = res_guard.release();
+    return CC_OK;
+}
+
+extern "C" cc_status cc_enumerate(const cc_graph *g, const cc_options *opt, cc_result **out)
+{
+    u64 need = 0;
+    cc_status s = enumerate_impl(g, opt, out, &need);
+    if (s == CC_ERR_CAPACITY && need > 0 && opt && opt->collect && opt->collect_capacity == 0) {
+        // automatic collect capacity: run again with exactly the capacity needed (the rerun
+        // starts from zeroed counters, so nothing is counted twice)
+        cc_options o2 = *opt;
+        o2.collect_capacity = need;
+        s = enumerate_impl(g, &o2, out, &need);
+    }
+    return s;
+}
+
+extern "C" cc_status cc_count_by_length(const cc_result *r, uint64_t *counts, size_t cap, size_t *n_lengths,
+                                        uint64_t *set_hash)
+{
+    if (!r)
+        return fail(CC_ERR_INVALID_ARGUMENT, "result is NULL");
+    const size_t need = (size_t)r->n + 1;
+    if (n_lengths)
+        *n_lengths = need;
+    if (set_hash)
+        *set_hash = r->hash;
+    if (counts == nullptr && cap == 0)
+        return CC_OK;
+    if (!counts || cap < need)
+        return fail(CC_ERR_BUFFER_TOO_SMALL, "counts needs n+1 = " + std::to_string(need) + " entries");
+    std::copy(r->counts.begin(), r->counts.begin() + need, counts);
+    return CC_OK;
+}
+
+extern "C" cc_status cc_paths_by_length(const cc_result *r, uint64_t *paths, size_t cap, size_t *n_lengths)
+{
+    if (!r)
+        return fail(CC_ERR_INVALID_ARGUMENT, "result is NULL");
+    const size_t need = (size_t)r->n + 1;
+    if (n_lengths)
+        *n_lengths = need;
+    if (paths == nullptr && cap == 0)
+        return CC_OK;
+    if (!paths || cap < need)
+        return fail(CC_ERR_BUFFER_TOO_SMALL, "paths needs n+1 = " + std::to_string(need) + " entries");
+    std::copy(r->paths.begin(), r->paths.begin() + need, paths);
+    return CC_OK;
+}
+
+extern "C" cc_status cc_num_stored_cycles(const cc_result *r, uint64_t *n)
+{
+    if (!r || !n)
+        return fail(CC_ERR_INVALID_ARGUMENT, "NULL argument");
+    *n = r->collected ? r->n_cyc : 0;
+    return CC_OK;
+}
+
+extern "C" cc_status cc_result_stats(const cc_result *r, cc_stats *out)
+{
+    if (!r || !out)
+        return fail(CC_ERR_INVALID_ARGUMENT, "NULL argument");
+    const uint32_t sz = out->struct_size;
+    if (sz < sizeof(uint32_t) || sz > sizeof(cc_stats))
+        return fail(CC_ERR_INVALID_ARGUMENT, "cc_stats.struct_size mismatch");
+    std::memcpy(out, &r->stats, sz);
+    out->struct_size = sz;
+    return CC_OK;
+}
+
+extern "C" cc_status cc_fetch_cycles(const cc_result *r, uint64_t first, uint64_t max_cycles, int32_t *vertices,
+                                     size_t vertices_cap, uint64_t *offsets, uint64_t *n_fetched)
+{
+    if (!r || !offsets || !n_fetched)
+        return fail(CC_ERR_INVALID_ARGUMENT, "NULL argument");
+    if (!r->collected)
+        return fail(CC_ERR_NOT_COLLECTED, "result was enumerated in count-only mode");
+    *n_fetched = 0;
+    if (first >= r->n_cyc || max_cycles == 0) {
+        offsets[0] = 0;
+        return CC_OK;
+    }
+    const u64 cnt = std::min<u64>(max_cycles, r->n_cyc - first);
+    int cur = -1;
+    CC_CUDA(cudaGetDevice(&cur));
+    CC_CUDA(cudaSetDevice(r->device));
+    struct Restore {
+        int d;
+        ~Restore()
+        {
+            if (d >= 0)
+                cudaSetDevice(d);
+        }
+    } restore{cur};
+    cudaStream_t st = nullptr;
+    uint32_t *d_len = nullptr;
+    CC_CUDA(cudaMalloc(&d_len, cnt * 4));
+    std::vector<uint32_t> len(cnt);
+    cudaError_t e = cc::launch_cycle_lengths(r->cyc, r->nw, first, cnt, d_len, st);
+    if (e == cudaSuccess)
+        e = cudaMemcpy(len.data(), d_len, cnt * 4, cudaMemcpyDeviceToHost);
+    cudaFree(d_len);
+    if (e != cudaSuccess)
+        return cuda_fail(e, "cycle lengths");
+    offsets[0] = 0;
+    for (u64 i = 0; i < cnt; ++i)
+        offsets[i + 1] = offsets[i] + len[i];
+    const u64 total = offsets[cnt];
+    if (total > vertices_cap || !vertices)
+        return fail(CC_ERR_BUFFER_TOO_SMALL, "vertices needs " + std::to_string(total) + " entries");
+    u64 *d_off = nullptr;
+    int32_t *d_v = nullptr;
+    CC_CUDA(cudaMalloc(&d_off, (cnt + 1) * 8));
+    e = cudaMalloc(&d_v, std::max<u64>(total, 1) * 4);
+    if (e == cudaSuccess)
+        e = cudaMemcpy(d_off, offsets, (cnt + 1) * 8, cudaMemcpyHostToDevice);
+    if (e == cudaSuccess)
+        e = cc::launch_cycle_sequences(r->cyc, r->nw, r->adj, r->orig, first, cnt, d_off, d_v, st);
+    if (e == cudaSuccess)
+        e = cudaMemcpy(vertices, d_v, total * 4, cudaMemcpyDeviceToHost);
+    cudaFree(d_off);
+    cudaFree(d_v);
+    if (e != cudaSuccess)
+        return cuda_fail(e, "cycle sequences");
+    *n_fetched = cnt;
+    return CC_OK;
+}

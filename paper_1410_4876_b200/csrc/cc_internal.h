@@ -1,0 +1,119 @@
+// cc_internal.h -- types shared by the host orchestrator (cc_host.cpp) and the sm_100a
+// kernels (cc_kernels.cu).  Not part of the public ABI (include/chordless.h is).
+#pragma once
+
+#include <cstdint>
+#include <cuda_runtime.h>
+
+namespace cc {
+
+typedef unsigned long long u64;
+
+// Size class of the bitmap-record path: S (Fig. 2) as NW 64-bit words.
+constexpr int kMaxWords = 8;           // n <= 512
+constexpr int kIdBits = 10;            // packed ids v1 | v2 << 10 | vt << 20 (n <= 1024)
+constexpr uint32_t kIdMask = (1u << kIdBits) - 1;
+constexpr int kBlock = 256;            // threads per CTA for every kernel
+// R: paths per thread per tile in k_expand_thread
+__host__ __device__ constexpr int expand_paths_per_thread(int nw) { return nw <= 4 ? 2 : 1; }
+constexpr int kMinLogPage = 10;        // pages hold >= kBlock * R records (one CTA tile)
+constexpr int kByteTableWords = 2;     // byte-wise key tables (H-spec keysum) for NW <= 2
+
+// Graph in device memory.  Internal vertex id == degree label (the host relabels), so the
+// label gate l(v) > l(v2) of Alg. 3 line 11 is the integer test v > v2 and
+// every adjacency row is sorted by label.
+struct DevGraph {
+    int32_t n;
+    int32_t nw;                  // words per bitmap row
+    const uint32_t *rowptr;      // [n+1]  V_e
+    const uint32_t *col;         // [2m]   E_e, rows ascending
+    const uint32_t *fwd;         // [n]    index in row u of the first neighbour w > u
+    const u64 *pair_prefix;      // [n+1]  prefix sums of C(d+(u), 2), d+(u) = |{w ~ u: w > u}|
+    const u64 *adj;              // [n*nw] adjacency bit rows
+    const u64 *key;              // [n]    key(v) = mix(seed ^ original id)   (H-spec)
+    const u64 *keybyte;          // [8*nw][256] (nw <= 2): sum of key(8j+i) over the set bits i of
+                                 //        byte value b at byte position j of S
+    const int32_t *orig;         // [n]    internal id -> original id
+};
+
+// Two record formats ("modes") for a path p = <v1..vt>:
+//   S-mode (collect mode):  RW = NW words  = the path bitmap S (Fig. 2)
+//   B-mode (count mode, the hot path): RW = NW + 1 words
+//        words 0..NW-1 = the blocked-vertex set B(p) = union of the closed neighbourhoods
+//                        N[v_i] of the interior vertices v_2..v_{t-1}
+//        word  NW      = keysum(p) = sum of key(v) over the vertices of p (H-spec)
+// plus, in both modes, ids = v1 | v2 << 10 | vt << 20 (the vectors V1, V2, VL).
+//
+// The frontier arena is split into pages of P = 2^log_p records.  Inside a page, records are
+// stored structure-of-arrays:
+//   word w of slot j : ((u64*)(base + page * page_bytes))[w * P + j]
+//   ids of slot j    : ((uint32_t*)(base + page * page_bytes + RW*P*8))[j]
+// A launch reads the virtual records [0, n_in) of the page list in_pages (record r lives in
+// page in_pages[r >> log_p], slot r & (P-1); every page but the last is full) and appends to
+// the virtual positions [out_off, out_off + out_cap) of out_pages.
+struct Pages {
+    char *base;
+    u64 page_bytes;
+    uint32_t log_p;
+    const uint32_t *in_pages;
+    const uint32_t *out_pages;
+};
+
+// Collect mode: closed cycles (bitmap S + {v}, v1 | v2 << 10).
+struct CycleStore {
+    u64 *s;
+    uint32_t *ids;
+    uint64_t cap;
+    u64 *count;                  // device counter (keeps counting past cap)
+};
+
+// Per-launch scratch accumulators (zeroed before, read back after every launch, so a launch
+// that overflows its output can be discarded without touching the totals).
+struct Scratch {
+    u64 out_count;               // records demanded by this launch (keeps counting past out_cap)
+    u64 err;                     // bit 0: output overflow
+    u64 cycles;                  // closures counted by this launch (all of one length)
+    u64 hash;                    // sum of h(C) over those closures (mod 2^64)
+    u64 cand;                    // candidate slots scanned
+    u64 cyc_count;               // collect-mode store counter (NOT reset per launch)
+};
+
+struct LaunchArgs {
+    DevGraph g;
+    Pages pg;
+    CycleStore cyc;
+    Scratch *sc;
+    uint64_t in_lo;              // Stage 1 only: pair range [in_lo, in_lo + n_in)
+    uint64_t n_in;               // input records (or pairs)
+    uint64_t out_off;            // first virtual output position in out_pages
+    uint64_t out_cap;            // positions available from out_off
+    int32_t emit;                // 1 = write extended paths / triplets
+    int32_t count;               // 1 = this shard owns (counts) the closures of this launch
+    int32_t collect;             // 1 = store closed cycles
+    int32_t filter;              // 1 = keep only records of this shard (Stage 1 / filter kernel)
+    uint64_t root_stride;        // Stage-1 root sample (0/1 = all)
+    uint64_t root_offset;
+    uint32_t shard_index;
+    uint32_t shard_count;
+};
+
+enum class ExpandVariant { Thread, Warp };
+
+enum class Mode { S, B };
+inline int record_words(int nw, Mode m) { return m == Mode::B ? nw + 1 : nw; }
+
+cudaError_t launch_stage1(const LaunchArgs &a, Mode m, cudaStream_t st, int grid_cap);
+cudaError_t launch_expand(const LaunchArgs &a, Mode m, ExpandVariant v, cudaStream_t st, int grid_cap);
+cudaError_t launch_shard_filter(const LaunchArgs &a, Mode m, cudaStream_t st, int grid_cap);
+cudaError_t launch_keys(u64 *key, u64 *keybyte, const int32_t *orig, int n, int nw, u64 seed,
+                        cudaStream_t st);
+cudaError_t launch_cycle_lengths(const CycleStore &c, int nw, uint64_t first, uint64_t count,
+                                 uint32_t *len, cudaStream_t st);
+cudaError_t launch_cycle_sequences(const CycleStore &c, int nw, const u64 *adj, const int32_t *orig,
+                                   uint64_t first, uint64_t count, const u64 *offsets,
+                                   int32_t *out, cudaStream_t st);
+// Resident CTAs per SM at kBlock threads with the given dynamic smem.
+// which: 0 = Stage 1, 1 = expand (thread), 2 = expand (warp), 3 = shard filter
+int max_blocks_per_sm(int which, Mode m, int nw, size_t smem);
+
+}  // namespace cc

@@ -1,0 +1,258 @@
+"""GPU parity: the CUDA path (through the C ABI) against the CPU oracle, element by element.
+
+Integer method: every comparison is bit-exact -- per-length counts, the 64-bit set
+hash, |F_t| per level, candidate slots, and (collect mode) the canonical cycle sequences.
+"""
+import math
+import os
+
+import numpy as np
+import pytest
+
+import oracle
+from paper_1410_4876_b200 import binding, build, inputs as I
+from tests import brute
+
+pytestmark = pytest.mark.gpu
+
+NT = os.cpu_count() or 1
+
+
+@pytest.fixture(scope="module")
+def ws():
+    import torch
+    assert torch.cuda.is_available()
+    build.build()
+    binding.load()
+    return torch.empty(1 << 30, dtype=torch.uint8, device="cuda")
+
+
+def gpu(g, ws, **kw):
+    return binding.enumerate_cycles(*g, workspace=ws, **kw)
+
+
+def assert_same(got, want, paths=True):
+    assert got["counts"].tolist() == want["counts"].tolist()
+    assert got["set_hash"] == want["set_hash"]
+    if paths:
+        assert got["paths_by_len"].tolist() == want["paths_by_len"].tolist()
+        assert got["candidates"] == want["candidates"]
+
+
+SMALL = [
+    ("p4x4", I.grid(4, 4)), ("p3x5", I.grid(3, 5)), ("k3x4", I.complete_bipartite(3, 4)),
+    ("k5", I.complete(5)), ("k12", I.complete(12)), ("c3", I.cycle(3)), ("c7", I.cycle(7)),
+    ("w6", I.wheel(6)), ("w3", I.wheel(3)), ("fig1", I.fig1_graph()), ("path5", I.path(5)),
+    ("star4", I.star(4)), ("tree40", I.random_tree(40, 3)), ("empty5", I.edges_to_csr(5, [])),
+    ("empty0", I.edges_to_csr(0, [])), ("one", I.edges_to_csr(1, [])), ("edge", I.edges_to_csr(2, [(0, 1)])),
+    ("two_triangles", I.edges_to_csr(7, [(0, 1), (1, 2), (2, 0), (4, 5), (5, 6), (6, 4)])),
+] + [(f"gnp{n}_{p}_{s}", I.gnp(n, p, 7000 + 31 * n + s)) for n in (8, 12, 16, 24) for p in (0.2, 0.35, 0.5)
+     for s in range(2)]
+
+
+@pytest.mark.parametrize("name,g", SMALL, ids=[s[0] for s in SMALL])
+def test_small_graphs_collect(ws, name, g):
+    got = gpu(g, ws, collect=True)
+    want = oracle.enumerate_cycles(*g, collect=True)
+    assert_same(got, want)
+    # same labelling (lowest-id ties) on both sides -> identical canonical sequences
+    assert sorted(map(tuple, got["cycles"])) == sorted(map(tuple, want["cycles"]))
+
+
+def test_p4x4_config0_full_list_vs_brute_force(ws):
+    """BASELINE configs[0]: P4xP4 full chordless-cycle list vs oracle and brute force."""
+    g = I.grid(4, 4)
+    got = gpu(g, ws, collect=True)
+    assert {k: int(v) for k, v in enumerate(got["counts"]) if v} == {4: 9, 8: 4, 10: 4, 12: 7}
+    assert {frozenset(c) for c in got["cycles"]} == brute.chordless_cycles_brute(*g)
+    assert got["set_hash"] == brute.hspec_hash(brute.chordless_cycles_brute(*g))
+
+
+TABLE1 = [("C_100", I.cycle(100), 1), ("Wheel_100", I.wheel(100), 101),
+          ("K_8_8", I.complete_bipartite(8, 8), 784), ("K_50_50", I.complete_bipartite(50, 50), 1500625),
+          ("Grid_4x10", I.grid(4, 10), 1823), ("Grid_5x6", I.grid(5, 6), 749),
+          ("Grid_5x10", I.grid(5, 10), 52620), ("Grid_6x6", I.grid(6, 6), 3436),
+          ("Grid_6x10", I.grid(6, 10), 800139), ("Grid_7x10", I.grid(7, 10), 8136453)]
+
+
+@pytest.mark.parametrize("name,g,total", TABLE1, ids=[t[0] for t in TABLE1])
+def test_table1_graphs(ws, name, g, total):
+    """Table 1 synthetic rows: totals from the paper, everything else
+    (per-length counts, hash, |F_t|, candidates) from the oracle."""
+    got = gpu(g, ws)
+    assert int(got["counts"].sum()) == total
+    assert_same(got, oracle.enumerate_cycles(*g, nthreads=NT))
+
+
+def test_k150_config1(ws):
+    """BASELINE configs[1]: K_{150,150} -> C(150,2)^2 = 124,880,625 4-cycles; |F_3| = 1,113,775
+    and 167,066,250 candidate slots; hash vs oracle."""
+    g = I.complete_bipartite(150, 150)
+    got = gpu(g, ws)
+    assert int(got["counts"][4]) == math.comb(150, 2) ** 2 == int(got["counts"].sum())
+    assert int(got["paths_by_len"][3]) == 1113775
+    assert got["candidates"] == 167066250
+    assert_same(got, oracle.enumerate_cycles(*g, nthreads=NT))
+
+
+def test_p8x8_config2(ws):
+    """BASELINE configs[2]: P8x8, full enumeration; N4..N12 closed forms + oracle."""
+    g = I.grid(8, 8)
+    got = gpu(g, ws)
+    c = got["counts"]
+    assert [int(c[k]) for k in (4, 6, 8, 10, 12)] == [49, 0, 36, 60, 223]
+    assert_same(got, oracle.enumerate_cycles(*g, nthreads=NT))
+
+
+@pytest.mark.parametrize("K", [14, 18, 22])
+def test_p10x10_config4_capped(ws, K):
+    """BASELINE configs[4] at full graph size with a length cap (the oracle finishes in < 1 s):
+    per-length counts, hash and |F_t| for k <= K; N4..N12 closed forms."""
+    g = I.grid(10, 10)
+    got = gpu(g, ws, max_len=K)
+    c = got["counts"]
+    assert [int(c[k]) for k in (4, 6, 8, 10, 12)] == [81, 0, 64, 112, 439]
+    assert_same(got, oracle.enumerate_cycles(*g, max_len=K, nthreads=NT))
+
+
+@pytest.mark.parametrize("K", [3, 4, 5, 6, 7])
+def test_gnp_dense_capped(ws, K):
+    """G(n, p) with n in the bitmap class (n = 500 -> 8 words) and a length cap."""
+    g = I.gnp(500, 0.02, 11)
+    assert_same(gpu(g, ws, max_len=K), oracle.enumerate_cycles(*g, max_len=K, nthreads=NT))
+
+
+@pytest.mark.parametrize("n", [63, 64, 65, 127, 128, 129, 191, 200, 256, 300, 383, 448, 511, 512])
+def test_word_boundaries(ws, n):
+    """Every bitmap width NW = 1..8 and the word boundaries (vertex 63/64 etc.)."""
+    g = I.gnp(n, 3.0 / n, 100 + n)
+    assert_same(gpu(g, ws, max_len=12), oracle.enumerate_cycles(*g, max_len=12, nthreads=NT))
+
+
+def test_dense_random_warp_variant(ws):
+    """Delta > 32 selects the warp-per-path kernel; check it on a graph with long paths too."""
+    g = I.gnp(120, 0.35, 5)
+    assert int(np.diff(g[1]).max()) > 32
+    assert_same(gpu(g, ws, max_len=6), oracle.enumerate_cycles(*g, max_len=6, nthreads=NT))
+    g = I.wheel(60)
+    assert_same(gpu(g, ws), oracle.enumerate_cycles(*g))
+
+
+@pytest.mark.parametrize("K", [3, 4, 5, 8, 10, 13])
+def test_max_len(ws, K):
+    g = I.grid(5, 6)
+    assert_same(gpu(g, ws, max_len=K), oracle.enumerate_cycles(*g, max_len=K))
+
+
+@pytest.mark.parametrize("pages", [64, 96, 128, 4096])
+def test_chunked_scheduler_matches_level_synchronous(ws, pages):
+    """A small workspace forces the depth-first chunk scheduler (PAPER.md:455 future work);
+    results must be identical to the oracle.  P7xP8: n = 56 (12-byte records, 1024-record
+    pages of 12 KiB), peak frontier 444,975 paths -- 64..128 pages cannot hold it."""
+    import torch
+    g = I.grid(7, 8)
+    small = torch.empty(pages * 1024 * 12, dtype=torch.uint8, device="cuda")
+    got = binding.enumerate_cycles(*g, workspace=small)
+    st = got["stats"]
+    if pages <= 128:
+        assert st["chunks"] > st["rounds"]
+        assert st["peak_arena_records"] <= st["arena_capacity"] < 444975
+    want = oracle.enumerate_cycles(*g, nthreads=NT)
+    assert_same(got, want)
+    if pages in (64, 4096):
+        got_c = binding.enumerate_cycles(*g, workspace=small, collect=True)
+        want_c = oracle.enumerate_cycles(*g, collect=True)
+        assert sorted(map(tuple, got_c["cycles"])) == sorted(map(tuple, want_c["cycles"]))
+
+
+def test_chunked_k50(ws):
+    import torch
+    g = I.complete_bipartite(50, 50)
+    small = torch.empty(1 << 20, dtype=torch.uint8, device="cuda")
+    got = binding.enumerate_cycles(*g, workspace=small)
+    assert got["stats"]["chunks"] > 2
+    assert_same(got, oracle.enumerate_cycles(*g, nthreads=NT))
+
+
+def test_workspace_too_small_fails_loudly(ws):
+    import torch
+    small = torch.empty(64 * 12, dtype=torch.uint8, device="cuda")
+    with pytest.raises(binding.CCError) as ei:
+        binding.enumerate_cycles(*I.complete_bipartite(50, 50), workspace=small)
+    assert ei.value.kind == "CC_ERR_CAPACITY"
+
+
+@pytest.mark.parametrize("W", [2, 3, 8])
+@pytest.mark.parametrize("name,g", [("grid6x7", I.grid(6, 7)), ("k40", I.complete_bipartite(40, 40)),
+                                    ("gnp", I.gnp(200, 0.04, 3))])
+def test_shards_sum_to_the_whole(ws, W, name, g):
+    """Shard-sum invariance: running shard_index = 0..W-1 and summing gives the
+    unsharded counts, hash, |F_t| and candidates exactly."""
+    kw = dict(max_len=9) if name == "gnp" else {}
+    full = gpu(g, ws, **kw)
+    parts = [gpu(g, ws, shard_index=i, shard_count=W, min_shard_paths=16, **kw) for i in range(W)]
+    assert sum(p["counts"] for p in parts).tolist() == full["counts"].tolist()
+    assert sum(p["set_hash"] for p in parts) % (1 << 64) == full["set_hash"]
+    assert sum(p["paths_by_len"] for p in parts).tolist() == full["paths_by_len"].tolist()
+    assert sum(p["candidates"] for p in parts) == full["candidates"]
+    # every shard got real work
+    assert all(int(p["paths_by_len"].sum()) > 0 for p in parts)
+
+
+@pytest.mark.parametrize("stride", [2, 5, 9])
+def test_root_sampling_matches_oracle(ws, stride):
+    """Root samples are defined on original ids on both sides."""
+    g = I.grid(7, 7)
+    for off in range(stride):
+        got = gpu(g, ws, root_stride=stride, root_offset=off)
+        want = oracle.enumerate_cycles(*g, root_stride=stride, root_offset=off, nthreads=NT)
+        assert_same(got, want)
+
+
+def test_hash_seed(ws):
+    g = I.grid(5, 5)
+    assert_same(gpu(g, ws, hash_seed=99), oracle.enumerate_cycles(*g, seed=99))
+
+
+def test_unsorted_rows_and_permuted_ids(ws):
+    """Input normalisation + isomorphism: a permuted graph gives the permuted cycle sets."""
+    n, rp, col = I.grid(5, 5)
+    perm = np.random.default_rng(3).permutation(n)
+    g2 = I.permute(n, rp, col, perm)
+    a = gpu((n, rp, col), ws, collect=True)
+    b = gpu(g2, ws, collect=True)
+    assert {frozenset(int(perm[v]) for v in c) for c in a["cycles"]} == {frozenset(c) for c in b["cycles"]}
+    # shuffle each row
+    rng = np.random.default_rng(4)
+    col3 = col.copy()
+    for v in range(n):
+        rng.shuffle(col3[rp[v]:rp[v + 1]])
+    assert_same(gpu((n, rp, col3), ws), oracle.enumerate_cycles(n, rp, col))
+
+
+def test_too_large_graph_rejected(ws):
+    g = I.gnp(600, 0.01, 1)
+    with pytest.raises(binding.CCError) as ei:
+        gpu(g, ws)
+    assert ei.value.kind == "CC_ERR_TOO_LARGE"
+
+
+def test_repeat_runs_deterministic(ws):
+    g = I.grid(6, 6)
+    a = gpu(g, ws)
+    for _ in range(3):
+        assert_same(gpu(g, ws), a)
+
+
+def test_stats_accounting(ws):
+    """Frontier accounting: paths_expanded = sum |F_t|; bytes_alg =
+    record_bytes * (paths read + paths written); t_dev > 0."""
+    g = I.grid(6, 8)
+    r = gpu(g, ws, profile=True)
+    s = r["stats"]
+    f = r["paths_by_len"]
+    assert s["paths_expanded"] == int(f.sum())
+    written = int(f[4:].sum())  # every path of >= 4 vertices was written by an expansion
+    assert s["bytes_alg"] == s["record_bytes"] * (int(f.sum()) + written)
+    assert s["t_dev_ms"] > 0 and s["t_expand_ms"] > 0
+    assert s["total_cycles"] == int(r["counts"].sum())
