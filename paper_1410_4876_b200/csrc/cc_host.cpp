@@ -497,7 +497,9 @@ static cc_status enumerate_impl(const cc_graph *cg, const cc_options *opt_in, cc
             return s;
     }
     const int nw = g->nw;
-    const u64 rec_bytes = (u64)nw * 8 + 4;
+    // count mode runs on blocked-vertex records (B-mode); collect mode keeps the bitmap S
+    const cc::Mode mode = opt.collect ? cc::Mode::S : cc::Mode::B;
+    const u64 rec_bytes = (u64)cc::record_words(nw, mode) * 8 + 4;
     S.record_bytes = rec_bytes;
 
     // ---- frontier arena, split into pages of P = 2^lp records
@@ -575,9 +577,10 @@ static cc_status enumerate_impl(const cc_graph *cg, const cc_options *opt_in, cc
 
     const cc::ExpandVariant variant = g->max_deg <= 32 ? cc::ExpandVariant::Thread : cc::ExpandVariant::Warp;
     const size_t gsmem = ((size_t)n * (nw + 1) + (nw <= cc::kByteTableWords ? (size_t)8 * nw * 256 : 0)) * 8;
-    const int grid_s1 = cc::max_blocks_per_sm(0, nw, gsmem) * sms;
-    const int grid_ex = cc::max_blocks_per_sm(variant == cc::ExpandVariant::Thread ? 1 : 2, nw, gsmem) * sms;
-    const int grid_sf = cc::max_blocks_per_sm(3, nw, 0) * sms;
+    const int grid_s1 = cc::max_blocks_per_sm(0, mode, nw, gsmem) * sms;
+    const int grid_ex =
+        cc::max_blocks_per_sm(variant == cc::ExpandVariant::Thread ? 1 : 2, mode, nw, cc::expand_smem(mode, nw, (int)n)) * sms;
+    const int grid_sf = cc::max_blocks_per_sm(3, mode, nw, 0) * sms;
     const double maxfan = (double)std::max<int64_t>(g->max_deg - 1, 1);
     const uint32_t W = opt.shard_count;
     const u64 shard_threshold = (u64)(opt.min_shard_paths ? opt.min_shard_paths : 1024) * W;
@@ -633,11 +636,11 @@ static cc_status enumerate_impl(const cc_graph *cg, const cc_options *opt_in, cc
         if (opt.profile)
             CC_CUDA(cudaEventRecord(ea, st));
         if (kind == STAGE1)
-            CC_CUDA(cc::launch_stage1(a, st, grid_s1));
+            CC_CUDA(cc::launch_stage1(a, mode, st, grid_s1));
         else if (kind == EXPAND)
-            CC_CUDA(cc::launch_expand(a, variant, st, grid_ex));
+            CC_CUDA(cc::launch_expand(a, mode, variant, st, grid_ex));
         else
-            CC_CUDA(cc::launch_shard_filter(a, st, grid_sf));
+            CC_CUDA(cc::launch_shard_filter(a, mode, st, grid_sf));
         if (opt.profile)
             CC_CUDA(cudaEventRecord(eb, st));
         CC_CUDA(cudaMemcpyAsync(h_sc, d_sc, sizeof(cc::Scratch), cudaMemcpyDeviceToHost, st));

@@ -112,6 +112,8 @@ cudaError_t launch_cycle_lengths(const CycleStore &c, int nw, uint64_t first, ui
 cudaError_t launch_cycle_sequences(const CycleStore &c, int nw, const u64 *adj, const int32_t *orig,
                                    uint64_t first, uint64_t count, const u64 *offsets,
                                    int32_t *out, cudaStream_t st);
+// dynamic shared memory of the expansion kernel for (mode, nw, n)
+size_t expand_smem(Mode m, int nw, int n);
 // Resident CTAs per SM at kBlock threads with the given dynamic smem.
 // which: 0 = Stage 1, 1 = expand (thread), 2 = expand (warp), 3 = shard filter
 int max_blocks_per_sm(int which, Mode m, int nw, size_t smem);

@@ -1,28 +1,34 @@
 // cc_kernels.cu -- sm_100a kernels of the chordless-cycle hot path (arXiv 1410.4876).
 //
-//   k_stage1         Stage 1 (Alg. 2): seeds T(G) and triangles.  One thread
-//                    per forward-neighbour pair (u; x < y in N+(u)) -- the sum_u C(d+(u),2) real
-//                    pairs, not the paper's |V|*Delta^2 padded index space.
-//   k_expand_thread  Stage 2 (Alg. 3) for Delta <= 32: one thread per path,
-//                    loops over Adj(v_t); extensions appended with a block-aggregated
-//                    prefix-sum allocator (one atomicAdd per CTA tile; the paper's
-//                    "serialization in the index calculation").
-//   k_expand_warp    Stage 2 for Delta > 32: one warp per path, lanes scan the suffix of the
-//                    sorted CSR row of v_t that passes the label gate (coalesced), ballot/popc
-//                    warp-aggregated appends.
-//   k_shard_filter   multi-GPU: keep the paths whose content hash falls in this shard.
-//   k_keys           key(v) = mix(seed ^ original id) (H-spec).
-//   k_cycle_*        collect mode: canonical vertex order of stored cycles (the inverse of the
-//                    bitmap encoding, PAPER.md:193 / SPEC.md:216).
+//   k_stage1<NW,BM>       Stage 1 (Alg. 2): seeds T(G) and triangles.  One
+//                         thread per forward-neighbour pair (u; x < y in N+(u)) -- the
+//                         sum_u C(d+(u),2) real pairs, not the paper's |V|*Delta^2 padded index
+//                         space.
+//   k_expand_blocked<NW>  Stage 2 (Alg. 3), count mode (the hot path): one
+//                         thread per path on the blocked-vertex record (below); extensions are
+//                         appended with a block-aggregated prefix-sum allocator (one atomicAdd per
+//                         CTA tile: the paper's "serialization in the index calculation",
+//                         PAPER.md:227, 289); input tiles stream in through a TMA bulk-copy ring.
+//   k_expand_thread<NW>   Stage 2, collect mode (S-mode records), thread per path.
+//   k_expand_warp<NW>     Stage 2, collect mode, Delta > 32: one warp per path, lanes scan the
+//                         suffix of the sorted CSR row of v_t that passes the label gate
+//                         (coalesced), ballot/popc warp-aggregated appends.
+//   k_shard_filter<RW>    multi-GPU: keep the paths whose content hash falls in this shard.
+//   k_keys, k_keybyte     key(v) = mix(seed ^ original id) (H-spec) and its byte tables.
+//   k_cycle_*             collect mode: canonical vertex order of stored cycles (the inverse of
+//                         the bitmap encoding, PAPER.md:193 / SPEC.md:216).
 //
-// Per-candidate test (Alg. 3 lines 11-15), for path p = <v1..vt> with
-// bitmap S and v in Adj(vt):
-//   gate   v > v2 (label order == id order after relabelling) and v not in S
-//   X      = Adj(v) & S & ~{vt}          (NW word-ANDs against the adjacency bit row of v)
-//   extend iff X == {}                   (<p,v> is a chordless path -> F_{t+1})
-//   close  iff X == {v1}                 (<p,v> is a chordless cycle of t+1 vertices)
-//   else   a chord: discard.
-// This is the paper's dichotomy evaluated on the bitmap S.
+// The test of Alg. 3 lines 11-15 for p = <v1..vt> and v in Adj(vt):
+//   gate   l(v) > l(v2) (== v > v2 after relabelling) and v not in p
+//   extend iff v is adjacent to none of v1..v_{t-1}            -> <p,v> in F_{t+1}
+//   close  iff v is adjacent to v1 and to none of v2..v_{t-1}  -> chordless cycle <p,v>
+//   else   a chord: discard                           (the dichotomy of PAPER.md:57-64)
+// B-mode evaluates it for all candidates at once on the blocked set
+//   B(p) = N[v2] u ... u N[v_{t-1}]   (closed neighbourhoods; B contains every vertex of p)
+//   Cand  = Adj(vt) & {v > v2} & ~B,   Close = Cand & Adj(v1),   Ext = Cand & ~Adj(v1)
+//   child <p,v>: B' = B | N[vt], keysum' = keysum + key(v), ids' = (v1, v2, v).
+// S-mode evaluates it per candidate on the bitmap S: X = Adj(v) & S & ~{vt};
+//   extend iff X == {}, close iff X == {v1}.
 #include "cc_internal.h"
 
 namespace cc {
@@ -37,51 +43,55 @@ __device__ __forceinline__ u64 mix64(u64 x)
     return x ^ (x >> 31);
 }
 
+__device__ __forceinline__ uint32_t pack_ids(uint32_t v1, uint32_t v2, uint32_t vt)
+{
+    return v1 | (v2 << kIdBits) | (vt << (2 * kIdBits));
+}
+
+__device__ __forceinline__ u64 bit_in_word(int w, uint32_t v)
+{
+    return (w == (int)(v >> 6)) ? (1ull << (v & 63)) : 0ull;
+}
+
 // ---------------------------------------------------------------------------- paged records
-template <int NW>
-__device__ __forceinline__ u64 *page_words(const Pages &pg, uint32_t page)
+__device__ __forceinline__ char *page_ptr(const Pages &pg, uint32_t page)
 {
-    return (u64 *)(pg.base + (u64)page * pg.page_bytes);
+    return pg.base + (u64)page * pg.page_bytes;
 }
 
-template <int NW>
-__device__ __forceinline__ uint32_t *page_ids(const Pages &pg, uint32_t page)
-{
-    return (uint32_t *)(pg.base + (u64)page * pg.page_bytes + ((u64)NW << pg.log_p) * 8);
-}
-
-template <int NW>
-__device__ __forceinline__ void load_record(const Pages &pg, uint32_t page, uint32_t slot, u64 (&S)[NW],
+template <int RW>
+__device__ __forceinline__ void load_record(const Pages &pg, uint32_t page, uint32_t slot, u64 (&W)[RW],
                                             uint32_t &id)
 {
-    const u64 *w = page_words<NW>(pg, page);
+    const char *pp = page_ptr(pg, page);
+    const u64 *w = (const u64 *)pp;
 #pragma unroll
-    for (int k = 0; k < NW; ++k)
-        S[k] = w[((u64)k << pg.log_p) + slot];
-    id = page_ids<NW>(pg, page)[slot];
+    for (int k = 0; k < RW; ++k)
+        W[k] = w[((u64)k << pg.log_p) + slot];
+    id = ((const uint32_t *)(pp + ((u64)RW << pg.log_p) * 8))[slot];
 }
 
-// write record at virtual output position o (page out_pages[o >> log_p])
-template <int NW>
-__device__ __forceinline__ void store_record(const Pages &pg, u64 o, const u64 (&S)[NW], uint32_t v,
-                                             bool add_v, uint32_t id)
+// write a record at virtual output position o (page out_pages[o >> log_p])
+template <int RW>
+__device__ __forceinline__ void store_record(const Pages &pg, u64 o, const u64 (&W)[RW], uint32_t id)
 {
     const uint32_t page = pg.out_pages[o >> pg.log_p];
     const uint32_t slot = (uint32_t)(o & ((1ull << pg.log_p) - 1));
-    u64 *w = page_words<NW>(pg, page);
+    char *pp = page_ptr(pg, page);
+    u64 *w = (u64 *)pp;
 #pragma unroll
-    for (int k = 0; k < NW; ++k)
-        w[((u64)k << pg.log_p) + slot] = S[k] | ((add_v && k == (int)(v >> 6)) ? (1ull << (v & 63)) : 0ull);
-    page_ids<NW>(pg, page)[slot] = id;
+    for (int k = 0; k < RW; ++k)
+        w[((u64)k << pg.log_p) + slot] = W[k];
+    ((uint32_t *)(pp + ((u64)RW << pg.log_p) * 8))[slot] = id;
 }
 
-template <int NW>
-__device__ __forceinline__ u64 shard_hash(const u64 (&S)[NW], uint32_t id)
+template <int RW>
+__device__ __forceinline__ u64 shard_hash(const u64 (&W)[RW], uint32_t id)
 {
     u64 h = mix64((u64)id);
 #pragma unroll
-    for (int w = 0; w < NW; ++w)
-        h = mix64(h ^ S[w]);
+    for (int w = 0; w < RW; ++w)
+        h = mix64(h ^ W[w]);
     return h;
 }
 
@@ -99,7 +109,7 @@ __device__ __forceinline__ u64 block_reserve(unsigned int c, u64 *counter, Reser
     unsigned int incl = c;
 #pragma unroll
     for (int o = 1; o < 32; o <<= 1) {
-        unsigned int v = __shfl_up_sync(FULL_MASK, incl, o);
+        const unsigned int v = __shfl_up_sync(FULL_MASK, incl, o);
         if (lane >= o)
             incl += v;
     }
@@ -107,11 +117,11 @@ __device__ __forceinline__ u64 block_reserve(unsigned int c, u64 *counter, Reser
         sm.warp[wid] = incl;
     __syncthreads();
     if (wid == 0) {
-        unsigned int w = lane < kBlock / 32 ? sm.warp[lane] : 0u;
+        const unsigned int w = lane < kBlock / 32 ? sm.warp[lane] : 0u;
         unsigned int wi = w;
 #pragma unroll
         for (int o = 1; o < 32; o <<= 1) {
-            unsigned int v = __shfl_up_sync(FULL_MASK, wi, o);
+            const unsigned int v = __shfl_up_sync(FULL_MASK, wi, o);
             if (lane >= o)
                 wi += v;
         }
@@ -205,7 +215,7 @@ __host__ __device__ constexpr int keybyte_words()
     return NW <= kByteTableWords ? 8 * NW * 256 : 0;
 }
 
-template <int NW>
+template <int NW, bool KB = true>
 __device__ __forceinline__ void stage_graph(const DevGraph &g, u64 *s_adj, u64 *s_key, u64 *s_kb)
 {
     const int nrow = g.n * NW;
@@ -213,14 +223,49 @@ __device__ __forceinline__ void stage_graph(const DevGraph &g, u64 *s_adj, u64 *
         s_adj[i] = g.adj[i];
     for (int i = threadIdx.x; i < g.n; i += blockDim.x)
         s_key[i] = g.key[i];
-    for (int i = threadIdx.x; i < keybyte_words<NW>(); i += blockDim.x)
-        s_kb[i] = g.keybyte[i];
+    if (KB)
+        for (int i = threadIdx.x; i < keybyte_words<NW>(); i += blockDim.x)
+            s_kb[i] = g.keybyte[i];
     __syncthreads();
 }
 
-__device__ __forceinline__ uint32_t pack_ids(uint32_t v1, uint32_t v2, uint32_t vt)
+// ---------------------------------------------------------------------------- TMA / mbarrier
+__device__ __forceinline__ uint32_t smem_u32(const void *p)
 {
-    return v1 | (v2 << kIdBits) | (vt << (2 * kIdBits));
+    return (uint32_t)__cvta_generic_to_shared(p);
+}
+
+__device__ __forceinline__ void mbar_init(u64 *bar, uint32_t count)
+{
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+
+__device__ __forceinline__ void mbar_arrive_expect_tx(u64 *bar, uint32_t bytes)
+{
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
+                 : "memory");
+}
+
+__device__ __forceinline__ void mbar_wait(u64 *bar, uint32_t parity)
+{
+    asm volatile(
+        "{\n"
+        " .reg .pred p;\n"
+        "WAIT_%=:\n"
+        " mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+        " @!p bra WAIT_%=;\n"
+        "}\n" ::"r"(smem_u32(bar)),
+        "r"(parity)
+        : "memory");
+}
+
+// 1-D bulk copy global -> shared through the TMA unit, completing bytes on the mbarrier
+__device__ __forceinline__ void tma_load_1d(void *dst, const void *src, uint32_t bytes, u64 *bar)
+{
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                     smem_u32(dst)),
+                 "l"(src), "r"(bytes), "r"(smem_u32(bar))
+                 : "memory");
 }
 
 template <int NW>
@@ -231,15 +276,16 @@ __device__ __forceinline__ void store_cycle(const LaunchArgs &p, const u64 (&S)[
     if (idx < p.cyc.cap) {
 #pragma unroll
         for (int w = 0; w < NW; ++w)
-            p.cyc.s[(u64)w * p.cyc.cap + idx] = S[w] | (w == (int)(v >> 6) ? (1ull << (v & 63)) : 0ull);
+            p.cyc.s[(u64)w * p.cyc.cap + idx] = S[w] | bit_in_word(w, v);
         p.cyc.ids[idx] = v1 | (v2 << kIdBits);
     }
 }
 
 // ---------------------------------------------------------------------------- Stage 1
-template <int NW>
+template <int NW, bool BM>
 __global__ void __launch_bounds__(kBlock) k_stage1(const LaunchArgs p)
 {
+    constexpr int RW = BM ? NW + 1 : NW;
     extern __shared__ u64 smem[];
     u64 *s_adj = smem;
     u64 *s_key = smem + p.g.n * NW;
@@ -252,7 +298,7 @@ __global__ void __launch_bounds__(kBlock) k_stage1(const LaunchArgs p)
     for (u64 base = (u64)blockIdx.x * kBlock; base < p.n_in; base += stride) {
         const u64 r = base + threadIdx.x;
         unsigned int emit = 0;
-        u64 S[NW];
+        u64 W[RW];
         uint32_t id = 0;
         if (r < p.n_in) {
             const u64 gid = p.in_lo + r;
@@ -277,17 +323,18 @@ __global__ void __launch_bounds__(kBlock) k_stage1(const LaunchArgs p)
             const uint32_t f = p.g.fwd[u];
             const uint32_t x = p.g.col[f + (uint32_t)i];
             const uint32_t y = p.g.col[f + (uint32_t)j];  // u < x < y in label order (Alg. 2 l.12)
-#pragma unroll
-            for (int w = 0; w < NW; ++w)
-                S[w] = (w == (int)(x >> 6) ? 1ull << (x & 63) : 0ull) |
-                       (w == (int)(u >> 6) ? 1ull << (u & 63) : 0ull);
             const bool tri = (s_adj[x * NW + (y >> 6)] >> (y & 63)) & 1ull;  // x in Adj(y) (l.13)
             if (tri) {
                 if (p.count) {  // Alg. 2 line 14: a triangle goes straight to C
                     cnt++;
                     hs += mix64(s_key[x] + s_key[u] + s_key[y]);
-                    if (p.collect)
+                    if (p.collect) {
+                        u64 S[NW];
+#pragma unroll
+                        for (int w = 0; w < NW; ++w)
+                            S[w] = bit_in_word(w, x) | bit_in_word(w, u);
                         store_cycle<NW>(p, S, y, x, u);
+                    }
                 }
             } else if (p.emit) {  // Alg. 2 line 15: <x,u,y> in T(G)
                 emit = 1;
@@ -296,12 +343,19 @@ __global__ void __launch_bounds__(kBlock) k_stage1(const LaunchArgs p)
                                      (u64)p.g.orig[y];
                     emit = (mix64(rkey) % p.root_stride) == p.root_offset;
                 }
+                if (BM) {  // B(<x,u,y>) = N[u]; keysum = key(x) + key(u) + key(y)
 #pragma unroll
-                for (int w = 0; w < NW; ++w)
-                    S[w] |= (w == (int)(y >> 6) ? 1ull << (y & 63) : 0ull);
+                    for (int w = 0; w < NW; ++w)
+                        W[w] = s_adj[u * NW + w] | bit_in_word(w, u);
+                    W[RW - 1] = s_key[x] + s_key[u] + s_key[y];
+                } else {  // S = {x, u, y}
+#pragma unroll
+                    for (int w = 0; w < NW; ++w)
+                        W[w] = bit_in_word(w, x) | bit_in_word(w, u) | bit_in_word(w, y);
+                }
                 id = pack_ids(x, u, y);
                 if (emit && p.filter)
-                    emit = (shard_hash<NW>(S, id) % p.shard_count) == p.shard_index;
+                    emit = (shard_hash<RW>(W, id) % p.shard_count) == p.shard_index;
             }
         }
         const u64 off = block_reserve(emit, &p.sc->out_count, rs);
@@ -309,133 +363,82 @@ __global__ void __launch_bounds__(kBlock) k_stage1(const LaunchArgs p)
             if (off >= p.out_cap)
                 p.sc->err = 1;
             else
-                store_record<NW>(p.pg, p.out_off + off, S, 0, false, id);
+                store_record<RW>(p.pg, p.out_off + off, W, id);
         }
     }
     flush_accum(cnt, hs, 0, p.sc);
 }
 
-// ---------------------------------------------------------------------------- Stage 2
-// Evaluate candidate v for path (S, v1, vt): 1 = extend, 2 = close, 0 = reject.
-template <int NW>
-__device__ __forceinline__ int classify(const u64 (&S)[NW], const u64 *s_adj, uint32_t v,
-                                        uint32_t v1, uint32_t vt)
-{
-    if ((word_of<NW>(S, v) >> (v & 63)) & 1ull)  // v in p (Alg. 3 line 11)
-        return 0;
-    bool ext = true, close = true;
-#pragma unroll
-    for (int w = 0; w < NW; ++w) {
-        u64 x = s_adj[v * NW + w] & S[w];
-        if (w == (int)(vt >> 6))
-            x &= ~(1ull << (vt & 63));
-        const u64 b1 = (w == (int)(v1 >> 6)) ? (1ull << (v1 & 63)) : 0ull;
-        ext &= (x == 0ull);
-        close &= (x == b1);
-    }
-    return ext ? 1 : (close ? 2 : 0);
-}
+// ---------------------------------------------------------------------------- Stage 2, B-mode
+// Persistent CTAs; the input tiles (kBlock*R consecutive records of one page: RW contiguous
+// word arrays + the ids array) stream into a kStages-deep shared-memory ring through TMA bulk
+// copies (cp.async.bulk + mbarrier), issued by thread 0 kStages tiles ahead of the consumers.
+constexpr int kStages = 4;
 
-// Bitset form of the per-path step for the thread-per-path kernel.  With S the path bitmap:
-//   cand = Adj(vt) & ~S & {v > v2}                 (Alg. 3 line 11 gate, all candidates at once)
-//   for v in cand:  X = Adj(v) & S & ~{vt}          (line 12 / 14 adjacency tests)
-//       X == {}   -> extension <p, v>               (line 15)
-//       X == {v1} -> chordless cycle <p, v>         (line 13)
-// Returns the extension vertices as a bitset; closures are counted and hashed here.
 template <int NW>
-__device__ __forceinline__ void expand_path(const LaunchArgs &p, const u64 (&S)[NW], uint32_t id,
-                                            const u64 *s_adj, const u64 *s_key, const u64 *s_kb,
-                                            u64 (&ext)[NW], u64 &cnt, u64 &hs, u64 &cand_slots)
+__host__ __device__ constexpr size_t blocked_stage_bytes()
 {
-    const uint32_t v1 = id & kIdMask;
-    const uint32_t v2 = (id >> kIdBits) & kIdMask;
-    const uint32_t vt = id >> (2 * kIdBits);
-    const u64 *av = s_adj + vt * NW;
-    u64 cand[NW];
-    const int lo = (int)v2 + 1;  // first label passing the gate
-#pragma unroll
-    for (int w = 0; w < NW; ++w) {
-        const u64 a = av[w];
-        cand_slots += __popcll(a);  // deg(vt): the candidate slots of Alg. 3 (stat only)
-        const int sh = lo - 64 * w;
-        const u64 above = sh <= 0 ? ~0ull : (sh >= 64 ? 0ull : (~0ull << sh));
-        cand[w] = a & ~S[w] & above;
-        ext[w] = 0;
-    }
-    u64 ks = 0;
-    bool have_ks = false;
-#pragma unroll
-    for (int w = 0; w < NW; ++w) {
-        while (cand[w]) {
-            const int b = __ffsll((long long)cand[w]) - 1;
-            cand[w] &= cand[w] - 1;
-            const uint32_t v = (uint32_t)(64 * w + b);
-            const u64 *ar = s_adj + v * NW;
-            bool e = true, c = true;
-#pragma unroll
-            for (int u = 0; u < NW; ++u) {
-                u64 x = ar[u] & S[u];
-                if (u == (int)(vt >> 6))
-                    x &= ~(1ull << (vt & 63));
-                const u64 b1 = (u == (int)(v1 >> 6)) ? (1ull << (v1 & 63)) : 0ull;
-                e &= (x == 0ull);
-                c &= (x == b1);
-            }
-            if (e) {
-                ext[w] |= 1ull << b;
-            } else if (c && p.count) {
-                ++cnt;
-                if (!have_ks) {
-                    ks = keysum<NW>(S, s_key, s_kb);
-                    have_ks = true;
-                }
-                hs += mix64(ks + s_key[v]);
-                if (p.collect)
-                    store_cycle<NW>(p, S, v, v1, v2);
-            }
-        }
-    }
+    return (size_t)kBlock * expand_paths_per_thread(NW) * ((NW + 1) * 8 + 4);
 }
 
 template <int NW>
-__global__ void __launch_bounds__(kBlock, NW <= 2 ? 4 : 2) k_expand_thread(const LaunchArgs p)
+__global__ void __launch_bounds__(kBlock, NW <= 2 ? 3 : 2) k_expand_blocked(const LaunchArgs p)
 {
-    // paths per thread per tile (2 for the long-path grid class NW <= 2, 1 for wide bitmaps):
-    // with the register double buffer this keeps NW <= 2 at 64 registers, 4 CTAs per SM
+    constexpr int RW = NW + 1;
     constexpr int R = expand_paths_per_thread(NW);
-    extern __shared__ u64 smem[];
-    u64 *s_adj = smem;
-    u64 *s_key = smem + p.g.n * NW;
-    u64 *s_kb = s_key + p.g.n;
+    constexpr int kTile = kBlock * R;
+    constexpr uint32_t kStageBytes = (uint32_t)blocked_stage_bytes<NW>();
+    extern __shared__ __align__(128) u64 smem[];
+    // ring first (16-byte aligned bulk-copy destinations), then the graph tables
+    char *ring = (char *)smem;
+    u64 *s_adj = (u64 *)(ring + (size_t)kStages * kStageBytes);
+    u64 *s_key = s_adj + p.g.n * NW;
     __shared__ ReserveSmem rs;
-    stage_graph<NW>(p.g, s_adj, s_key, s_kb);
+    __shared__ __align__(8) u64 bar[kStages];
 
-    const u64 pmask = (1ull << p.pg.log_p) - 1;
-    constexpr u64 kTile = (u64)kBlock * R;
-    const u64 stride = (u64)gridDim.x * kTile;
-    u64 cnt = 0, hs = 0, cand = 0;
-
-    // a tile of kBlock*R records never straddles a page (pages hold >= kTile records);
-    // thread j takes records base + j + kBlock*i, i < R (each load instruction coalesced).
-    // Register double buffering: the next tile's loads are in flight during this tile's work.
-    u64 S[R][NW], Sn[R][NW];
-    uint32_t id[R], idn[R];
-    auto load_tile = [&](u64 base, u64 (&T)[R][NW], uint32_t (&I)[R]) {
+    const u64 n_tiles = (p.n_in + kTile - 1) / kTile;
+    const u64 my_tiles = blockIdx.x < n_tiles ? (n_tiles - 1 - blockIdx.x) / gridDim.x + 1 : 0;
+    // tile k of this CTA -> global tile blockIdx.x + k * gridDim.x -> its page and slot
+    auto issue = [&](u64 k) {
+        const int st = (int)(k % kStages);
+        const u64 base = (blockIdx.x + k * gridDim.x) * (u64)kTile;
         const uint32_t page = p.pg.in_pages[base >> p.pg.log_p];
-        const uint32_t slot0 = (uint32_t)(base & pmask) + threadIdx.x;
+        const uint32_t slot0 = (uint32_t)(base & ((1ull << p.pg.log_p) - 1));
+        const char *pp = p.pg.base + (u64)page * p.pg.page_bytes;
+        char *dst = ring + (size_t)st * kStageBytes;
+        mbar_arrive_expect_tx(&bar[st], kStageBytes);
+#pragma unroll
+        for (int w = 0; w < RW; ++w)
+            tma_load_1d(dst + (size_t)w * kTile * 8, pp + (((u64)w << p.pg.log_p) + slot0) * 8, kTile * 8,
+                        &bar[st]);
+        tma_load_1d(dst + (size_t)RW * kTile * 8, pp + ((u64)RW << p.pg.log_p) * 8 + (u64)slot0 * 4, kTile * 4,
+                    &bar[st]);
+    };
+    if (threadIdx.x == 0) {
+        for (int st = 0; st < kStages; ++st)
+            mbar_init(&bar[st], 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+        for (u64 k = 0; k < my_tiles && k < (u64)kStages; ++k)
+            issue(k);
+    }
+    stage_graph<NW, false>(p.g, s_adj, s_key, nullptr);  // includes __syncthreads
+
+    u64 cnt = 0, hs = 0, cand = 0;
+    for (u64 k = 0; k < my_tiles; ++k) {
+        const int st = (int)(k % kStages);
+        const u64 base = (blockIdx.x + k * gridDim.x) * (u64)kTile;
+        mbar_wait(&bar[st], (uint32_t)((k / kStages) & 1));
+        const char *buf = ring + (size_t)st * kStageBytes;
+        u64 W[R][RW];
+        uint32_t id[R];
 #pragma unroll
         for (int i = 0; i < R; ++i) {
-            I[i] = 0xffffffffu;
-            if (base + threadIdx.x + (u64)kBlock * i < p.n_in)
-                load_record<NW>(p.pg, page, slot0 + kBlock * i, T[i], I[i]);
+            const int j = threadIdx.x + kBlock * i;
+#pragma unroll
+            for (int w = 0; w < RW; ++w)
+                W[i][w] = ((const u64 *)buf)[w * kTile + j];
+            id[i] = base + j < p.n_in ? ((const uint32_t *)(buf + (size_t)RW * kTile * 8))[j] : 0xffffffffu;
         }
-    };
-    u64 base = (u64)blockIdx.x * kTile;
-    if (base < p.n_in)
-        load_tile(base, S, id);
-    for (; base < p.n_in; base += stride) {
-        if (base + stride < p.n_in)
-            load_tile(base + stride, Sn, idn);
         u64 ext[R][NW];
         unsigned int ne = 0;
 #pragma unroll
@@ -445,11 +448,158 @@ __global__ void __launch_bounds__(kBlock, NW <= 2 ? 4 : 2) k_expand_thread(const
                 ext[i][w] = 0;
             if (id[i] == 0xffffffffu)
                 continue;
-            expand_path<NW>(p, S[i], id[i], s_adj, s_key, s_kb, ext[i], cnt, hs, cand);
-            if (p.emit) {
+            const uint32_t v1 = id[i] & kIdMask;
+            const uint32_t v2 = (id[i] >> kIdBits) & kIdMask;
+            const uint32_t vt = id[i] >> (2 * kIdBits);
+            const int lo = (int)v2 + 1;  // first label passing the gate
+            u64 close[NW];
+            bool any_close = false;
 #pragma unroll
-                for (int w = 0; w < NW; ++w)
-                    ne += __popcll(ext[i][w]);
+            for (int w = 0; w < NW; ++w) {
+                const u64 a = s_adj[vt * NW + w];
+                cand += __popcll(a);  // deg(vt): the candidate slots of Alg. 3 (statistic)
+                const int sh = lo - 64 * w;
+                const u64 above = sh <= 0 ? ~0ull : (sh >= 64 ? 0ull : (~0ull << sh));
+                const u64 c = a & above & ~W[i][w];
+                const u64 a1 = s_adj[v1 * NW + w];
+                close[w] = c & a1;
+                ext[i][w] = p.emit ? (c & ~a1) : 0ull;
+                any_close |= close[w] != 0ull;
+                ne += __popcll(ext[i][w]);
+            }
+            if (any_close && p.count) {
+                const u64 ks = W[i][NW];
+#pragma unroll
+                for (int w = 0; w < NW; ++w) {
+                    u64 m = close[w];
+                    cnt += __popcll(m);
+                    while (m) {
+                        const int b = __ffsll((long long)m) - 1;
+                        m &= m - 1;
+                        hs += mix64(ks + s_key[64 * w + b]);
+                    }
+                }
+            }
+        }
+        // every thread has read stage st (block_reserve starts with a barrier) -> refill it
+        const u64 off = block_reserve(ne, &p.sc->out_count, rs);
+        if (threadIdx.x == 0 && k + kStages < my_tiles) {
+            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+            issue(k + kStages);
+        }
+        if (ne) {
+            if (off + ne > p.out_cap) {
+                p.sc->err = 1;
+            } else {
+                u64 o = p.out_off + off;
+#pragma unroll
+                for (int i = 0; i < R; ++i) {
+                    bool any = false;
+#pragma unroll
+                    for (int w = 0; w < NW; ++w)
+                        any |= ext[i][w] != 0ull;
+                    if (!any)
+                        continue;
+                    // the child's blocked set: vt becomes interior -> B | N[vt]
+                    const uint32_t vt = id[i] >> (2 * kIdBits);
+                    const uint32_t v12 = id[i] & ((1u << (2 * kIdBits)) - 1);
+                    u64 C[RW];
+#pragma unroll
+                    for (int w = 0; w < NW; ++w)
+                        C[w] = W[i][w] | s_adj[vt * NW + w] | bit_in_word(w, vt);
+                    const u64 ks = W[i][NW];
+#pragma unroll
+                    for (int w = 0; w < NW; ++w) {
+                        u64 m = ext[i][w];
+                        while (m) {
+                            const int b = __ffsll((long long)m) - 1;
+                            m &= m - 1;
+                            const uint32_t v = (uint32_t)(64 * w + b);
+                            C[NW] = ks + s_key[v];
+                            store_record<RW>(p.pg, o++, C, v12 | (v << (2 * kIdBits)));
+                        }
+                    }
+                }
+            }
+        }
+    }
+    if (!p.count)
+        cand = 0;
+    flush_accum(cnt, hs, cand, p.sc);
+}
+
+// ---------------------------------------------------------------------------- Stage 2, S-mode
+// Per-candidate form on the bitmap S (collect mode): cand = Adj(vt) & ~S & {v > v2};
+// for v in cand: X = Adj(v) & S & ~{vt}; X == {} -> extension, X == {v1} -> cycle.
+template <int NW>
+__global__ void __launch_bounds__(kBlock) k_expand_thread(const LaunchArgs p)
+{
+    extern __shared__ u64 smem[];
+    u64 *s_adj = smem;
+    u64 *s_key = smem + p.g.n * NW;
+    u64 *s_kb = s_key + p.g.n;
+    __shared__ ReserveSmem rs;
+    stage_graph<NW>(p.g, s_adj, s_key, s_kb);
+
+    const u64 pmask = (1ull << p.pg.log_p) - 1;
+    u64 cnt = 0, hs = 0, cand = 0;
+    const u64 stride = (u64)gridDim.x * kBlock;
+    for (u64 base = (u64)blockIdx.x * kBlock; base < p.n_in; base += stride) {
+        const u64 r = base + threadIdx.x;
+        u64 S[NW], ext[NW];
+        uint32_t id = 0;
+        unsigned int ne = 0;
+#pragma unroll
+        for (int w = 0; w < NW; ++w)
+            ext[w] = 0;
+        if (r < p.n_in) {
+            load_record<NW>(p.pg, p.pg.in_pages[base >> p.pg.log_p], (uint32_t)(r & pmask), S, id);
+            const uint32_t v1 = id & kIdMask;
+            const uint32_t v2 = (id >> kIdBits) & kIdMask;
+            const uint32_t vt = id >> (2 * kIdBits);
+            u64 cw[NW];
+            const int lo = (int)v2 + 1;
+#pragma unroll
+            for (int w = 0; w < NW; ++w) {
+                const u64 a = s_adj[vt * NW + w];
+                cand += __popcll(a);
+                const int sh = lo - 64 * w;
+                const u64 above = sh <= 0 ? ~0ull : (sh >= 64 ? 0ull : (~0ull << sh));
+                cw[w] = a & ~S[w] & above;
+            }
+            u64 ks = 0;
+            bool have_ks = false;
+#pragma unroll
+            for (int w = 0; w < NW; ++w) {
+                while (cw[w]) {
+                    const int b = __ffsll((long long)cw[w]) - 1;
+                    cw[w] &= cw[w] - 1;
+                    const uint32_t v = (uint32_t)(64 * w + b);
+                    bool e = true, c = true;
+#pragma unroll
+                    for (int u = 0; u < NW; ++u) {
+                        u64 x = s_adj[v * NW + u] & S[u];
+                        if (u == (int)(vt >> 6))
+                            x &= ~(1ull << (vt & 63));
+                        e &= (x == 0ull);
+                        c &= (x == bit_in_word(u, v1));
+                    }
+                    if (e) {
+                        if (p.emit) {
+                            ext[w] |= 1ull << b;
+                            ++ne;
+                        }
+                    } else if (c && p.count) {
+                        ++cnt;
+                        if (!have_ks) {
+                            ks = keysum<NW>(S, s_key, s_kb);
+                            have_ks = true;
+                        }
+                        hs += mix64(ks + s_key[v]);
+                        if (p.collect)
+                            store_cycle<NW>(p, S, v, v1, v2);
+                    }
+                }
             }
         }
         const u64 off = block_reserve(ne, &p.sc->out_count, rs);
@@ -458,28 +608,21 @@ __global__ void __launch_bounds__(kBlock, NW <= 2 ? 4 : 2) k_expand_thread(const
                 p.sc->err = 1;
             } else {
                 u64 o = p.out_off + off;
+                const uint32_t v12 = id & ((1u << (2 * kIdBits)) - 1);
 #pragma unroll
-                for (int i = 0; i < R; ++i) {
-                    const uint32_t v12 = id[i] & ((1u << (2 * kIdBits)) - 1);
+                for (int w = 0; w < NW; ++w) {
+                    while (ext[w]) {
+                        const int b = __ffsll((long long)ext[w]) - 1;
+                        ext[w] &= ext[w] - 1;
+                        const uint32_t v = (uint32_t)(64 * w + b);
+                        u64 C[NW];
 #pragma unroll
-                    for (int w = 0; w < NW; ++w) {
-                        u64 m = ext[i][w];
-                        while (m) {
-                            const int b = __ffsll((long long)m) - 1;
-                            m &= m - 1;
-                            const uint32_t v = (uint32_t)(64 * w + b);
-                            store_record<NW>(p.pg, o++, S[i], v, true, v12 | (v << (2 * kIdBits)));
-                        }
+                        for (int u = 0; u < NW; ++u)
+                            C[u] = S[u] | bit_in_word(u, v);
+                        store_record<NW>(p.pg, o++, C, v12 | (v << (2 * kIdBits)));
                     }
                 }
             }
-        }
-#pragma unroll
-        for (int i = 0; i < R; ++i) {
-            id[i] = idn[i];
-#pragma unroll
-            for (int w = 0; w < NW; ++w)
-                S[i][w] = Sn[i][w];
         }
     }
     if (!p.count)
@@ -493,8 +636,7 @@ __global__ void __launch_bounds__(kBlock) k_expand_warp(const LaunchArgs p)
     extern __shared__ u64 smem[];
     u64 *s_adj = smem;
     u64 *s_key = smem + p.g.n * NW;
-    u64 *s_kb = s_key + p.g.n;
-    stage_graph<NW>(p.g, s_adj, s_key, s_kb);
+    stage_graph<NW>(p.g, s_adj, s_key, s_key + p.g.n);
 
     const int lane = threadIdx.x & 31;
     const unsigned int lt_mask = (1u << lane) - 1u;
@@ -528,7 +670,18 @@ __global__ void __launch_bounds__(kBlock) k_expand_warp(const LaunchArgs p)
             uint32_t v = 0;
             if (k < k2) {
                 v = __ldg(col + k);
-                c = classify<NW>(S, s_adj, v, v1, vt);
+                if (!((word_of<NW>(S, v) >> (v & 63)) & 1ull)) {  // v not in p
+                    bool e = true, cl = true;
+#pragma unroll
+                    for (int w = 0; w < NW; ++w) {
+                        u64 x = s_adj[v * NW + w] & S[w];
+                        if (w == (int)(vt >> 6))
+                            x &= ~(1ull << (vt & 63));
+                        e &= (x == 0ull);
+                        cl &= (x == bit_in_word(w, v1));
+                    }
+                    c = e ? 1 : (cl ? 2 : 0);
+                }
             }
             const unsigned int eb = __ballot_sync(FULL_MASK, c == 1 && p.emit);
             if (eb) {
@@ -538,10 +691,15 @@ __global__ void __launch_bounds__(kBlock) k_expand_warp(const LaunchArgs p)
                 b = __shfl_sync(FULL_MASK, b, 0);
                 if (c == 1) {
                     const u64 off = b + __popc(eb & lt_mask);
-                    if (off >= p.out_cap)
+                    if (off >= p.out_cap) {
                         p.sc->err = 1;
-                    else
-                        store_record<NW>(p.pg, p.out_off + off, S, v, true, pack_ids(v1, v2, v));
+                    } else {
+                        u64 C[NW];
+#pragma unroll
+                        for (int w = 0; w < NW; ++w)
+                            C[w] = S[w] | bit_in_word(w, v);
+                        store_record<NW>(p.pg, p.out_off + off, C, pack_ids(v1, v2, v));
+                    }
                 }
             }
             // the keysum of S is needed once per path: computed by the whole warp (lane w < NW
@@ -580,7 +738,7 @@ __global__ void __launch_bounds__(kBlock) k_expand_warp(const LaunchArgs p)
 }
 
 // ---------------------------------------------------------------------------- shard filter
-template <int NW>
+template <int RW>
 __global__ void __launch_bounds__(kBlock) k_shard_filter(const LaunchArgs p)
 {
     __shared__ ReserveSmem rs;
@@ -588,19 +746,19 @@ __global__ void __launch_bounds__(kBlock) k_shard_filter(const LaunchArgs p)
     const u64 stride = (u64)gridDim.x * kBlock;
     for (u64 base = (u64)blockIdx.x * kBlock; base < p.n_in; base += stride) {
         const u64 r = base + threadIdx.x;
-        u64 S[NW];
+        u64 W[RW];
         uint32_t id = 0;
         unsigned int keep = 0;
         if (r < p.n_in) {
-            load_record<NW>(p.pg, p.pg.in_pages[base >> p.pg.log_p], (uint32_t)(r & pmask), S, id);
-            keep = (shard_hash<NW>(S, id) % p.shard_count) == p.shard_index;
+            load_record<RW>(p.pg, p.pg.in_pages[base >> p.pg.log_p], (uint32_t)(r & pmask), W, id);
+            keep = (shard_hash<RW>(W, id) % p.shard_count) == p.shard_index;
         }
         const u64 off = block_reserve(keep, &p.sc->out_count, rs);
         if (keep) {
             if (off >= p.out_cap)
                 p.sc->err = 1;
             else
-                store_record<NW>(p.pg, p.out_off + off, S, 0, false, id);
+                store_record<RW>(p.pg, p.out_off + off, W, id);
         }
     }
 }
@@ -643,9 +801,6 @@ __global__ void k_cycle_sequences(const CycleStore c, int nw, const u64 *adj, co
     const u64 i = (u64)blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= count)
         return;
-    u64 S[kMaxWords];
-    for (int w = 0; w < nw; ++w)
-        S[w] = c.s[(u64)w * c.cap + first + i];
     const uint32_t id = c.ids[first + i];
     uint32_t prev = id & kIdMask, cur = (id >> kIdBits) & kIdMask;
     const u64 o = offsets[i], k = offsets[i + 1] - offsets[i];
@@ -655,7 +810,7 @@ __global__ void k_cycle_sequences(const CycleStore c, int nw, const u64 *adj, co
     for (u64 j = 2; j < k; ++j) {
         uint32_t nxt = 0;
         for (int w = 0; w < nw; ++w) {
-            u64 x = adj[(u64)cur * nw + w] & S[w];
+            u64 x = adj[(u64)cur * nw + w] & c.s[(u64)w * c.cap + first + i];
             if (w == (int)(prev >> 6))
                 x &= ~(1ull << (prev & 63));
             if (x) {
@@ -670,18 +825,7 @@ __global__ void k_cycle_sequences(const CycleStore c, int nw, const u64 *adj, co
 }
 
 // ---------------------------------------------------------------------------- launchers
-#define CC_DISPATCH_NW(nw, KERNEL, ...)                \
-    switch (nw) {                                      \
-    case 1: KERNEL<1><<<__VA_ARGS__>>>(a); break;      \
-    case 2: KERNEL<2><<<__VA_ARGS__>>>(a); break;      \
-    case 3: KERNEL<3><<<__VA_ARGS__>>>(a); break;      \
-    case 4: KERNEL<4><<<__VA_ARGS__>>>(a); break;      \
-    case 5: KERNEL<5><<<__VA_ARGS__>>>(a); break;      \
-    case 6: KERNEL<6><<<__VA_ARGS__>>>(a); break;      \
-    case 7: KERNEL<7><<<__VA_ARGS__>>>(a); break;      \
-    case 8: KERNEL<8><<<__VA_ARGS__>>>(a); break;      \
-    default: return cudaErrorInvalidValue;             \
-    }
+#define CC_CASES(MAC) MAC(1) MAC(2) MAC(3) MAC(4) MAC(5) MAC(6) MAC(7) MAC(8)
 
 static inline size_t graph_smem(const LaunchArgs &a)
 {
@@ -689,30 +833,42 @@ static inline size_t graph_smem(const LaunchArgs &a)
     return ((size_t)a.g.n * (a.g.nw + 1) + kb) * sizeof(u64);
 }
 
-template <typename F>
-static cudaError_t set_smem(F *f, size_t smem)
+static size_t blocked_ring_bytes(int nw)
+{
+    switch (nw) {
+#define RB(N) case N: return (size_t)kStages * blocked_stage_bytes<N>();
+        CC_CASES(RB)
+#undef RB
+    }
+    return 0;
+}
+
+// dynamic shared memory of the expansion kernel for (mode, nw, n)
+size_t expand_smem(Mode m, int nw, int n)
+{
+    if (m == Mode::B)
+        return blocked_ring_bytes(nw) + (size_t)n * (nw + 1) * sizeof(u64);
+    const size_t kb = nw <= kByteTableWords ? (size_t)8 * nw * 256 : 0;
+    return ((size_t)n * (nw + 1) + kb) * sizeof(u64);
+}
+
+typedef void (*KernelFn)(const LaunchArgs);
+
+static cudaError_t set_smem(KernelFn f, size_t smem)
 {
     if (smem > 48 * 1024)
-        return cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        return cudaFuncSetAttribute((const void *)f, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     return cudaSuccess;
 }
 
-#define CC_SET_SMEM_NW(nw, KERNEL, smem)                                   \
-    do {                                                                   \
-        cudaError_t e_ = cudaSuccess;                                      \
-        switch (nw) {                                                      \
-        case 1: e_ = set_smem(KERNEL<1>, smem); break;                     \
-        case 2: e_ = set_smem(KERNEL<2>, smem); break;                     \
-        case 3: e_ = set_smem(KERNEL<3>, smem); break;                     \
-        case 4: e_ = set_smem(KERNEL<4>, smem); break;                     \
-        case 5: e_ = set_smem(KERNEL<5>, smem); break;                     \
-        case 6: e_ = set_smem(KERNEL<6>, smem); break;                     \
-        case 7: e_ = set_smem(KERNEL<7>, smem); break;                     \
-        case 8: e_ = set_smem(KERNEL<8>, smem); break;                     \
-        }                                                                  \
-        if (e_ != cudaSuccess)                                             \
-            return e_;                                                     \
-    } while (0)
+static cudaError_t run(KernelFn f, unsigned int grid, size_t smem, cudaStream_t st, const LaunchArgs &a)
+{
+    cudaError_t e = set_smem(f, smem);
+    if (e != cudaSuccess)
+        return e;
+    f<<<grid, kBlock, smem, st>>>(a);
+    return cudaGetLastError();
+}
 
 static inline unsigned int grid_for(u64 items_per_block, u64 n, int grid_cap)
 {
@@ -724,41 +880,70 @@ static inline unsigned int grid_for(u64 items_per_block, u64 n, int grid_cap)
     return (unsigned int)b;
 }
 
-cudaError_t launch_stage1(const LaunchArgs &a, cudaStream_t st, int grid_cap)
+// kernel for (which, mode, nw); which: 0 stage1, 1 expand thread, 2 expand warp, 3 filter
+static KernelFn kernel_for(int which, Mode m, int nw)
 {
-    if (a.n_in == 0)
-        return cudaSuccess;
-    const size_t smem = graph_smem(a);
-    CC_SET_SMEM_NW(a.g.nw, k_stage1, smem);
-    const unsigned int grid = grid_for(kBlock, a.n_in, grid_cap);
-    CC_DISPATCH_NW(a.g.nw, k_stage1, grid, kBlock, smem, st);
-    return cudaGetLastError();
-}
-
-cudaError_t launch_expand(const LaunchArgs &a, ExpandVariant v, cudaStream_t st, int grid_cap)
-{
-    if (a.n_in == 0)
-        return cudaSuccess;
-    const size_t smem = graph_smem(a);
-    if (v == ExpandVariant::Thread) {
-        CC_SET_SMEM_NW(a.g.nw, k_expand_thread, smem);
-        const unsigned int grid = grid_for((u64)kBlock * expand_paths_per_thread(a.g.nw), a.n_in, grid_cap);
-        CC_DISPATCH_NW(a.g.nw, k_expand_thread, grid, kBlock, smem, st);
-    } else {
-        CC_SET_SMEM_NW(a.g.nw, k_expand_warp, smem);
-        const unsigned int grid = grid_for(kBlock / 32, a.n_in, grid_cap);
-        CC_DISPATCH_NW(a.g.nw, k_expand_warp, grid, kBlock, smem, st);
+    const bool bm = m == Mode::B;
+    switch (which) {
+    case 0:
+#define K0(N) if (nw == N) return bm ? k_stage1<N, true> : k_stage1<N, false>;
+        CC_CASES(K0)
+#undef K0
+        break;
+    case 1:
+#define K1(N) if (nw == N) return bm ? k_expand_blocked<N> : k_expand_thread<N>;
+        CC_CASES(K1)
+#undef K1
+        break;
+    case 2:
+#define K2(N) if (nw == N) return bm ? k_expand_blocked<N> : k_expand_warp<N>;
+        CC_CASES(K2)
+#undef K2
+        break;
+    default: {
+        const int rw = record_words(nw, m);
+#define K3(N) if (rw == N) return k_shard_filter<N>;
+        CC_CASES(K3) K3(9)
+#undef K3
     }
-    return cudaGetLastError();
+    }
+    return nullptr;
 }
 
-cudaError_t launch_shard_filter(const LaunchArgs &a, cudaStream_t st, int grid_cap)
+cudaError_t launch_stage1(const LaunchArgs &a, Mode m, cudaStream_t st, int grid_cap)
 {
     if (a.n_in == 0)
         return cudaSuccess;
-    const unsigned int grid = grid_for(kBlock, a.n_in, grid_cap);
-    CC_DISPATCH_NW(a.g.nw, k_shard_filter, grid, kBlock, 0, st);
-    return cudaGetLastError();
+    KernelFn f = kernel_for(0, m, a.g.nw);
+    if (!f)
+        return cudaErrorInvalidValue;
+    return run(f, grid_for(kBlock, a.n_in, grid_cap), graph_smem(a), st, a);
+}
+
+cudaError_t launch_expand(const LaunchArgs &a, Mode m, ExpandVariant v, cudaStream_t st, int grid_cap)
+{
+    if (a.n_in == 0)
+        return cudaSuccess;
+    const int which = v == ExpandVariant::Thread ? 1 : 2;
+    KernelFn f = kernel_for(which, m, a.g.nw);
+    if (!f)
+        return cudaErrorInvalidValue;
+    u64 per_block = kBlock;
+    if (m == Mode::B)
+        per_block = (u64)kBlock * expand_paths_per_thread(a.g.nw);
+    else if (v == ExpandVariant::Warp)
+        per_block = kBlock / 32;
+    return run(f, grid_for(per_block, a.n_in, grid_cap), expand_smem(m, a.g.nw, a.g.n), st, a);
+}
+
+cudaError_t launch_shard_filter(const LaunchArgs &a, Mode m, cudaStream_t st, int grid_cap)
+{
+    if (a.n_in == 0)
+        return cudaSuccess;
+    KernelFn f = kernel_for(3, m, a.g.nw);
+    if (!f)
+        return cudaErrorInvalidValue;
+    return run(f, grid_for(kBlock, a.n_in, grid_cap), 0, st, a);
 }
 
 cudaError_t launch_keys(u64 *key, u64 *keybyte, const int32_t *orig, int n, int nw, u64 seed,
@@ -792,41 +977,16 @@ cudaError_t launch_cycle_sequences(const CycleStore &c, int nw, const u64 *adj, 
     return cudaGetLastError();
 }
 
-static cudaError_t raise_smem(int which, int nw, size_t smem)
+int max_blocks_per_sm(int which, Mode m, int nw, size_t smem)
 {
-    switch (which) {
-    case 0: CC_SET_SMEM_NW(nw, k_stage1, smem); break;
-    case 1: CC_SET_SMEM_NW(nw, k_expand_thread, smem); break;
-    case 2: CC_SET_SMEM_NW(nw, k_expand_warp, smem); break;
-    }
-    return cudaSuccess;
-}
-
-int max_blocks_per_sm(int which, int nw, size_t smem)
-{
-    int nb = 1;
-    cudaError_t e = cudaSuccess;
-#define CC_OCC(KERNEL)                                                                          \
-    switch (nw) {                                                                               \
-    case 1: e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, KERNEL<1>, kBlock, smem); break; \
-    case 2: e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, KERNEL<2>, kBlock, smem); break; \
-    case 3: e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, KERNEL<3>, kBlock, smem); break; \
-    case 4: e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, KERNEL<4>, kBlock, smem); break; \
-    case 5: e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, KERNEL<5>, kBlock, smem); break; \
-    case 6: e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, KERNEL<6>, kBlock, smem); break; \
-    case 7: e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, KERNEL<7>, kBlock, smem); break; \
-    case 8: e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, KERNEL<8>, kBlock, smem); break; \
-    }
-    if (smem > 48 * 1024 && raise_smem(which, nw, smem) != cudaSuccess)
+    KernelFn f = kernel_for(which, m, nw);
+    if (!f)
         return 1;
-    switch (which) {
-    case 0: CC_OCC(k_stage1); break;
-    case 1: CC_OCC(k_expand_thread); break;
-    case 2: CC_OCC(k_expand_warp); break;
-    default: CC_OCC(k_shard_filter); break;
-    }
-#undef CC_OCC
-    if (e != cudaSuccess || nb < 1)
+    const size_t sm = which == 3 ? 0 : smem;
+    int nb = 1;
+    if (set_smem(f, sm) != cudaSuccess)
+        return 1;
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, (const void *)f, kBlock, sm) != cudaSuccess || nb < 1)
         nb = 1;
     return nb;
 }
