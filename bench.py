@@ -241,16 +241,9 @@ def main():
     cyc_local = int(counts.sum())
     paths_local = int(paths.sum())
     if world > 1:
-        t = torch.tensor([dev_ms], dtype=torch.float64, device=dev)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        dev_ms = float(t.item())
-        v = torch.tensor(np.concatenate([counts.astype(np.int64), [np.int64(np.uint64(h).view(np.int64))],
-                                         [paths_local]]), dtype=torch.int64, device=dev)
-        dist.all_reduce(v, op=dist.ReduceOp.SUM)
-        v = v.cpu().numpy()
-        counts = v[:-2].astype(np.uint64)
-        h = int(np.int64(v[-2]).view(np.uint64))
-        paths_total = int(v[-1])
+        from paper_1410_4876_b200 import dist as D
+        dev_ms = D.max_over_ranks(dev_ms, device=dev)
+        counts, h, paths_total = D.combine_shards(counts, h, paths_local, device=dev)
     else:
         paths_total = paths_local
     cycles_total = int(counts.sum())
@@ -298,9 +291,8 @@ def main():
         torch.cuda.synchronize()
         el = time.perf_counter() - t0
         if world > 1:
-            t = torch.tensor([el], dtype=torch.float64, device=dev)
-            dist.all_reduce(t, op=dist.ReduceOp.MAX)
-            el = float(t.item())
+            from paper_1410_4876_b200 import dist as D
+            el = D.max_over_ranks(el, device=dev)
         e2e = {"value": cycles_total / (el / ne), "unit": UNIT, "h2d_bytes_per_step": h2d // ne,
                "d2h_bytes_per_step": d2h // ne, "ms_per_step": 1e3 * el / ne}
 

@@ -97,13 +97,15 @@ __device__ __forceinline__ u64 shard_hash(const u64 (&W)[RW], uint32_t id)
 
 // Block-wide exclusive scan of c plus one atomicAdd per CTA on *counter.  Must be called by
 // every thread of the block.  Returns this thread's first output index (relative to the
-// counter's origin).
+// counter's origin).  Two barriers; callers that reserve repeatedly alternate two ReserveSmem
+// buffers (tile parity) so no third barrier is needed before the buffer is reused.
 struct ReserveSmem {
     u64 base;
+    unsigned int total;
     unsigned int warp[kBlock / 32];
 };
 
-__device__ __forceinline__ u64 block_reserve(unsigned int c, u64 *counter, ReserveSmem &sm)
+__device__ __forceinline__ u64 block_reserve2(unsigned int c, u64 *counter, ReserveSmem &sm)
 {
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
     unsigned int incl = c;
@@ -127,14 +129,54 @@ __device__ __forceinline__ u64 block_reserve(unsigned int c, u64 *counter, Reser
         }
         if (lane < kBlock / 32)
             sm.warp[lane] = wi - w;
-        if (lane == kBlock / 32 - 1)
+        if (lane == kBlock / 32 - 1) {
+            sm.total = wi;
             sm.base = wi ? atomicAdd(counter, (u64)wi) : 0ull;
+        }
     }
     __syncthreads();
-    const u64 r = sm.base + sm.warp[wid] + (incl - c);
-    __syncthreads();  // sm is reused by the next tile
+    return sm.base + sm.warp[wid] + (incl - c);
+}
+
+// single-buffer form: a third barrier protects sm before its next use
+__device__ __forceinline__ u64 block_reserve(unsigned int c, u64 *counter, ReserveSmem &sm)
+{
+    const u64 r = block_reserve2(c, counter, sm);
+    __syncthreads();
     return r;
 }
+
+// Sequential appends at virtual output positions o, o+1, ...: the page's word-array base
+// pointers are resolved once and again only when o crosses into the next page.
+template <int RW>
+struct Appender {
+    u64 *w[RW];
+    uint32_t *ids;
+    uint32_t slot;
+    u64 o;
+    __device__ __forceinline__ void seek(const Pages &pg, u64 pos)
+    {
+        o = pos;
+        const uint32_t page = pg.out_pages[o >> pg.log_p];
+        slot = (uint32_t)(o & ((1ull << pg.log_p) - 1));
+        char *pp = pg.base + (u64)page * pg.page_bytes;
+#pragma unroll
+        for (int k = 0; k < RW; ++k)
+            w[k] = (u64 *)pp + ((u64)k << pg.log_p);
+        ids = (uint32_t *)(pp + ((u64)RW << pg.log_p) * 8);
+    }
+    __device__ __forceinline__ void put(const Pages &pg, const u64 (&W)[RW], uint32_t id)
+    {
+        if (slot >> pg.log_p)  // crossed into the next page
+            seek(pg, o);
+#pragma unroll
+        for (int k = 0; k < RW; ++k)
+            w[k][slot] = W[k];
+        ids[slot] = id;
+        ++slot;
+        ++o;
+    }
+};
 
 template <int NW>
 __device__ __forceinline__ u64 word_of(const u64 (&S)[NW], uint32_t v)
@@ -373,7 +415,7 @@ __global__ void __launch_bounds__(kBlock) k_stage1(const LaunchArgs p)
 // Persistent CTAs; the input tiles (kBlock*R consecutive records of one page: RW contiguous
 // word arrays + the ids array) stream into a kStages-deep shared-memory ring through TMA bulk
 // copies (cp.async.bulk + mbarrier), issued by thread 0 kStages tiles ahead of the consumers.
-constexpr int kStages = 4;
+constexpr int kStages = 3;
 
 template <int NW>
 __host__ __device__ constexpr size_t blocked_stage_bytes()
@@ -393,7 +435,13 @@ __global__ void __launch_bounds__(kBlock, NW <= 2 ? 3 : 2) k_expand_blocked(cons
     char *ring = (char *)smem;
     u64 *s_adj = (u64 *)(ring + (size_t)kStages * kStageBytes);
     u64 *s_key = s_adj + p.g.n * NW;
-    __shared__ ReserveSmem rs;
+    u64 *s_above = s_key + p.g.n;  // s_above[v*NW + w] = word w of {x : x > v} (the label gate)
+    // staged children of one tile: parent state per path slot, one (slot, v) entry per child
+    constexpr uint32_t kChildCap = 2 * kTile;  // overflow (> 2 children per path on average) falls back
+    u64 *s_par = s_above + p.g.n * NW;                    // [kTile][RW]
+    uint32_t *s_pid = (uint32_t *)(s_par + kTile * RW);   // [kTile]
+    uint32_t *s_child = s_pid + kTile;                    // [kChildCap]
+    __shared__ ReserveSmem rs[2];
     __shared__ __align__(8) u64 bar[kStages];
 
     const u64 n_tiles = (p.n_in + kTile - 1) / kTile;
@@ -420,6 +468,10 @@ __global__ void __launch_bounds__(kBlock, NW <= 2 ? 3 : 2) k_expand_blocked(cons
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
         for (u64 k = 0; k < my_tiles && k < (u64)kStages; ++k)
             issue(k);
+    }
+    for (int i = threadIdx.x; i < p.g.n * NW; i += kBlock) {
+        const int sh = i / NW + 1 - 64 * (i % NW);
+        s_above[i] = sh <= 0 ? ~0ull : (sh >= 64 ? 0ull : (~0ull << sh));
     }
     stage_graph<NW, false>(p.g, s_adj, s_key, nullptr);  // includes __syncthreads
 
@@ -451,16 +503,13 @@ __global__ void __launch_bounds__(kBlock, NW <= 2 ? 3 : 2) k_expand_blocked(cons
             const uint32_t v1 = id[i] & kIdMask;
             const uint32_t v2 = (id[i] >> kIdBits) & kIdMask;
             const uint32_t vt = id[i] >> (2 * kIdBits);
-            const int lo = (int)v2 + 1;  // first label passing the gate
             u64 close[NW];
             bool any_close = false;
 #pragma unroll
             for (int w = 0; w < NW; ++w) {
                 const u64 a = s_adj[vt * NW + w];
                 cand += __popcll(a);  // deg(vt): the candidate slots of Alg. 3 (statistic)
-                const int sh = lo - 64 * w;
-                const u64 above = sh <= 0 ? ~0ull : (sh >= 64 ? 0ull : (~0ull << sh));
-                const u64 c = a & above & ~W[i][w];
+                const u64 c = a & s_above[v2 * NW + w] & ~W[i][w];
                 const u64 a1 = s_adj[v1 * NW + w];
                 close[w] = c & a1;
                 ext[i][w] = p.emit ? (c & ~a1) : 0ull;
@@ -482,43 +531,89 @@ __global__ void __launch_bounds__(kBlock, NW <= 2 ? 3 : 2) k_expand_blocked(cons
             }
         }
         // every thread has read stage st (block_reserve starts with a barrier) -> refill it
-        const u64 off = block_reserve(ne, &p.sc->out_count, rs);
+        const u64 off = block_reserve2(ne, &p.sc->out_count, rs[k & 1]);
         if (threadIdx.x == 0 && k + kStages < my_tiles) {
             asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
             issue(k + kStages);
         }
-        if (ne) {
-            if (off + ne > p.out_cap) {
+        const u64 tile_base = rs[k & 1].base;  // first output position of this CTA tile
+        const unsigned int total = rs[k & 1].total;
+        if (off + ne > p.out_cap) {
+            if (ne)
                 p.sc->err = 1;
-            } else {
-                u64 o = p.out_off + off;
+        } else {
+            // Staged append.  Each path with children publishes its child state (B | N[vt],
+            // keysum, v1|v2) in s_par[slot]; each child gets one 4-byte entry (slot, v) at its
+            // tile-local position in s_child.  After a barrier all threads copy the tile's
+            // children to their consecutive output positions: a uniform, fully coalesced loop.
+            const uint32_t loc0 = (uint32_t)(off - tile_base);
+            uint32_t loc = loc0;
 #pragma unroll
-                for (int i = 0; i < R; ++i) {
-                    bool any = false;
+            for (int i = 0; i < R; ++i) {
+                bool any = false;
 #pragma unroll
-                    for (int w = 0; w < NW; ++w)
-                        any |= ext[i][w] != 0ull;
-                    if (!any)
-                        continue;
-                    // the child's blocked set: vt becomes interior -> B | N[vt]
-                    const uint32_t vt = id[i] >> (2 * kIdBits);
-                    const uint32_t v12 = id[i] & ((1u << (2 * kIdBits)) - 1);
+                for (int w = 0; w < NW; ++w)
+                    any |= ext[i][w] != 0ull;
+                if (!any)
+                    continue;
+                const uint32_t slot = threadIdx.x + kBlock * i;
+                const uint32_t vt = id[i] >> (2 * kIdBits);
+#pragma unroll
+                for (int w = 0; w < NW; ++w)
+                    s_par[slot * RW + w] = W[i][w] | s_adj[vt * NW + w] | bit_in_word(w, vt);
+                s_par[slot * RW + NW] = W[i][NW];
+                s_pid[slot] = id[i] & ((1u << (2 * kIdBits)) - 1);
+#pragma unroll
+                for (int w = 0; w < NW; ++w) {
+                    u64 m = ext[i][w];
+                    while (m) {
+                        const int b = __ffsll((long long)m) - 1;
+                        m &= m - 1;
+                        if (loc < kChildCap)
+                            s_child[loc] = slot | ((uint32_t)(64 * w + b) << 16);
+                        ++loc;
+                    }
+                }
+            }
+        }
+        __syncthreads();
+        {
+            if (total > kChildCap) {
+                // rare (Delta > 4 with many children): fall back to per-thread appends
+                if (ne && off + ne <= p.out_cap) {
+                    Appender<RW> out;
+                    out.seek(p.pg, p.out_off + off);
+#pragma unroll
+                    for (int i = 0; i < R; ++i) {
+                        const uint32_t vt = id[i] >> (2 * kIdBits);
+                        const uint32_t v12 = id[i] & ((1u << (2 * kIdBits)) - 1);
+                        u64 C[RW];
+#pragma unroll
+                        for (int w = 0; w < NW; ++w)
+                            C[w] = W[i][w] | s_adj[(vt & kIdMask) * NW + w] | bit_in_word(w, vt);
+#pragma unroll
+                        for (int w = 0; w < NW; ++w) {
+                            u64 m = ext[i][w];
+                            while (m) {
+                                const int b = __ffsll((long long)m) - 1;
+                                m &= m - 1;
+                                const uint32_t v = (uint32_t)(64 * w + b);
+                                C[NW] = W[i][NW] + s_key[v];
+                                out.put(p.pg, C, v12 | (v << (2 * kIdBits)));
+                            }
+                        }
+                    }
+                }
+            } else if (tile_base + total <= p.out_cap) {
+                for (unsigned int j = threadIdx.x; j < total; j += kBlock) {
+                    const uint32_t e = s_child[j];
+                    const uint32_t slot = e & 0xffffu, v = e >> 16;
                     u64 C[RW];
 #pragma unroll
                     for (int w = 0; w < NW; ++w)
-                        C[w] = W[i][w] | s_adj[vt * NW + w] | bit_in_word(w, vt);
-                    const u64 ks = W[i][NW];
-#pragma unroll
-                    for (int w = 0; w < NW; ++w) {
-                        u64 m = ext[i][w];
-                        while (m) {
-                            const int b = __ffsll((long long)m) - 1;
-                            m &= m - 1;
-                            const uint32_t v = (uint32_t)(64 * w + b);
-                            C[NW] = ks + s_key[v];
-                            store_record<RW>(p.pg, o++, C, v12 | (v << (2 * kIdBits)));
-                        }
-                    }
+                        C[w] = s_par[slot * RW + w];
+                    C[NW] = s_par[slot * RW + NW] + s_key[v];
+                    store_record<RW>(p.pg, p.out_off + tile_base + j, C, s_pid[slot] | (v << (2 * kIdBits)));
                 }
             }
         }
@@ -846,8 +941,11 @@ static size_t blocked_ring_bytes(int nw)
 // dynamic shared memory of the expansion kernel for (mode, nw, n)
 size_t expand_smem(Mode m, int nw, int n)
 {
-    if (m == Mode::B)
-        return blocked_ring_bytes(nw) + (size_t)n * (nw + 1) * sizeof(u64);
+    if (m == Mode::B) {
+        const size_t tile = (size_t)kBlock * expand_paths_per_thread(nw);
+        return blocked_ring_bytes(nw) + (size_t)n * (2 * nw + 1) * sizeof(u64) + tile * (nw + 1) * 8 + tile * 4 +
+               2 * tile * 4;
+    }
     const size_t kb = nw <= kByteTableWords ? (size_t)8 * nw * 256 : 0;
     return ((size_t)n * (nw + 1) + kb) * sizeof(u64);
 }
