@@ -12,7 +12,8 @@ import os
 import numpy as np
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libchordless.so")
+# CC_LIBCHORDLESS overrides the library path (A/B builds of the same ABI)
+LIB_PATH = os.environ.get("CC_LIBCHORDLESS") or os.path.join(HERE, "libchordless.so")
 
 CC_STATUS = {
     0: "CC_OK", 1: "CC_ERR_INVALID_ARGUMENT", 2: "CC_ERR_INVALID_VERTEX", 3: "CC_ERR_SELF_LOOP",

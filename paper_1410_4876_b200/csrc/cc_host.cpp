@@ -499,7 +499,9 @@ static cc_status enumerate_impl(const cc_graph *cg, const cc_options *opt_in, cc
     const int nw = g->nw;
     // count mode runs on blocked-vertex records (B-mode); collect mode keeps the bitmap S
     const cc::Mode mode = opt.collect ? cc::Mode::S : cc::Mode::B;
-    const u64 rec_bytes = (u64)cc::record_words(nw, mode) * 8 + 4;
+    // B-mode records carry v1, v2, vt in the spare top bits of the blocked set when n allows
+    const bool packed = mode == cc::Mode::B && cc::packable(nw, (int)n);
+    const u64 rec_bytes = (u64)cc::record_bytes(nw, mode, packed);
     S.record_bytes = rec_bytes;
 
     // ---- frontier arena, split into pages of P = 2^lp records
@@ -574,13 +576,18 @@ static cc_status enumerate_impl(const cc_graph *cg, const cc_options *opt_in, cc
     base.root_offset = opt.root_offset;
     base.shard_index = opt.shard_index;
     base.shard_count = opt.shard_count;
+    base.idb = (uint32_t)cc::id_bits((int)n);
+    base.packed = packed ? 1 : 0;
 
-    const cc::ExpandVariant variant = g->max_deg <= 32 ? cc::ExpandVariant::Thread : cc::ExpandVariant::Warp;
+    const cc::ExpandVariant variant = (mode == cc::Mode::B && g->max_deg <= 4) ? cc::ExpandVariant::Small
+                                      : g->max_deg <= 32                      ? cc::ExpandVariant::Thread
+                                                                              : cc::ExpandVariant::Warp;
     const size_t gsmem = ((size_t)n * (nw + 1) + (nw <= cc::kByteTableWords ? (size_t)8 * nw * 256 : 0)) * 8;
-    const int grid_s1 = cc::max_blocks_per_sm(0, mode, nw, gsmem) * sms;
+    const int grid_s1 = cc::max_blocks_per_sm(0, mode, nw, packed, gsmem) * sms;
     const int grid_ex =
-        cc::max_blocks_per_sm(variant == cc::ExpandVariant::Thread ? 1 : 2, mode, nw, cc::expand_smem(mode, nw, (int)n)) * sms;
-    const int grid_sf = cc::max_blocks_per_sm(3, mode, nw, 0) * sms;
+        cc::max_blocks_per_sm(variant == cc::ExpandVariant::Small ? 4 : variant == cc::ExpandVariant::Thread ? 1 : 2,
+                              mode, nw, packed, cc::expand_smem(mode, nw, (int)n, packed)) * sms;
+    const int grid_sf = cc::max_blocks_per_sm(3, mode, nw, packed, 0) * sms;
     const double maxfan = (double)std::max<int64_t>(g->max_deg - 1, 1);
     const uint32_t W = opt.shard_count;
     const u64 shard_threshold = (u64)(opt.min_shard_paths ? opt.min_shard_paths : 1024) * W;

@@ -95,13 +95,29 @@ struct LaunchArgs {
     uint64_t root_offset;
     uint32_t shard_index;
     uint32_t shard_count;
+    uint32_t idb;                // packed records: bits per id (ids in the top 3*idb bits of word NW-1)
+    uint32_t packed;             // 1 = B-mode record with packed ids (no ids array)
 };
 
-enum class ExpandVariant { Thread, Warp };
+// Thread: thread per path; Warp: warp per path (S-mode, Delta > 32); Small: B-mode with
+// Delta <= 4 (at most 3 children per path)
+enum class ExpandVariant { Thread, Warp, Small };
 
 enum class Mode { S, B };
 inline int record_words(int nw, Mode m) { return m == Mode::B ? nw + 1 : nw; }
+// B-mode records may carry v1, v2, vt in the unused top bits of the last blocked-set word
+// (bits >= n are never set in B): possible iff 64*nw - n >= 3*idb, idb = ceil(log2 n).
+inline int id_bits(int n)
+{
+    int b = 1;
+    while ((1 << b) < n)
+        ++b;
+    return b;
+}
+inline bool packable(int nw, int n) { return 64 * nw - n >= 3 * id_bits(n); }
+inline int record_bytes(int nw, Mode m, bool packed) { return record_words(nw, m) * 8 + (packed ? 0 : 4); }
 
+// a.packed selects the packed-ids record variants of the B-mode kernels
 cudaError_t launch_stage1(const LaunchArgs &a, Mode m, cudaStream_t st, int grid_cap);
 cudaError_t launch_expand(const LaunchArgs &a, Mode m, ExpandVariant v, cudaStream_t st, int grid_cap);
 cudaError_t launch_shard_filter(const LaunchArgs &a, Mode m, cudaStream_t st, int grid_cap);
@@ -112,10 +128,10 @@ cudaError_t launch_cycle_lengths(const CycleStore &c, int nw, uint64_t first, ui
 cudaError_t launch_cycle_sequences(const CycleStore &c, int nw, const u64 *adj, const int32_t *orig,
                                    uint64_t first, uint64_t count, const u64 *offsets,
                                    int32_t *out, cudaStream_t st);
-// dynamic shared memory of the expansion kernel for (mode, nw, n)
-size_t expand_smem(Mode m, int nw, int n);
+// dynamic shared memory of the expansion kernel for (mode, nw, n, packed)
+size_t expand_smem(Mode m, int nw, int n, bool packed);
 // Resident CTAs per SM at kBlock threads with the given dynamic smem.
-// which: 0 = Stage 1, 1 = expand (thread), 2 = expand (warp), 3 = shard filter
-int max_blocks_per_sm(int which, Mode m, int nw, size_t smem);
+// which: 0 = Stage 1, 1 = expand (thread), 2 = expand (warp), 3 = shard filter, 4 = expand (small)
+int max_blocks_per_sm(int which, Mode m, int nw, bool packed, size_t smem);
 
 }  // namespace cc

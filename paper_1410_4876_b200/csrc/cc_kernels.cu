@@ -59,7 +59,7 @@ __device__ __forceinline__ char *page_ptr(const Pages &pg, uint32_t page)
     return pg.base + (u64)page * pg.page_bytes;
 }
 
-template <int RW>
+template <int RW, bool IDS = true>
 __device__ __forceinline__ void load_record(const Pages &pg, uint32_t page, uint32_t slot, u64 (&W)[RW],
                                             uint32_t &id)
 {
@@ -68,11 +68,14 @@ __device__ __forceinline__ void load_record(const Pages &pg, uint32_t page, uint
 #pragma unroll
     for (int k = 0; k < RW; ++k)
         W[k] = w[((u64)k << pg.log_p) + slot];
-    id = ((const uint32_t *)(pp + ((u64)RW << pg.log_p) * 8))[slot];
+    if (IDS)
+        id = ((const uint32_t *)(pp + ((u64)RW << pg.log_p) * 8))[slot];
+    else
+        id = 0;
 }
 
 // write a record at virtual output position o (page out_pages[o >> log_p])
-template <int RW>
+template <int RW, bool IDS = true>
 __device__ __forceinline__ void store_record(const Pages &pg, u64 o, const u64 (&W)[RW], uint32_t id)
 {
     const uint32_t page = pg.out_pages[o >> pg.log_p];
@@ -82,7 +85,19 @@ __device__ __forceinline__ void store_record(const Pages &pg, u64 o, const u64 (
 #pragma unroll
     for (int k = 0; k < RW; ++k)
         w[((u64)k << pg.log_p) + slot] = W[k];
-    ((uint32_t *)(pp + ((u64)RW << pg.log_p) * 8))[slot] = id;
+    if (IDS)
+        ((uint32_t *)(pp + ((u64)RW << pg.log_p) * 8))[slot] = id;
+}
+
+// Packed B-mode ids: v1 | v2 << idb | vt << 2idb in the top 3*idb bits of word NW-1.
+__device__ __forceinline__ uint32_t packed_ids(u64 last_word, uint32_t idb)
+{
+    return (uint32_t)(last_word >> (64 - 3 * idb));
+}
+__device__ __forceinline__ u64 with_packed_ids(u64 last_word, uint32_t ids, uint32_t idb)
+{
+    const u64 low = (1ull << (64 - 3 * idb)) - 1;
+    return (last_word & low) | ((u64)ids << (64 - 3 * idb));
 }
 
 template <int RW>
@@ -165,16 +180,22 @@ struct Appender {
             w[k] = (u64 *)pp + ((u64)k << pg.log_p);
         ids = (uint32_t *)(pp + ((u64)RW << pg.log_p) * 8);
     }
-    __device__ __forceinline__ void put(const Pages &pg, const u64 (&W)[RW], uint32_t id)
+    template <bool IDS>
+    __device__ __forceinline__ void put_words(const Pages &pg, const u64 (&W)[RW], uint32_t id)
     {
         if (slot >> pg.log_p)  // crossed into the next page
             seek(pg, o);
 #pragma unroll
         for (int k = 0; k < RW; ++k)
             w[k][slot] = W[k];
-        ids[slot] = id;
+        if (IDS)
+            ids[slot] = id;
         ++slot;
         ++o;
+    }
+    __device__ __forceinline__ void put(const Pages &pg, const u64 (&W)[RW], uint32_t id)
+    {
+        put_words<true>(pg, W, id);
     }
 };
 
@@ -324,7 +345,7 @@ __device__ __forceinline__ void store_cycle(const LaunchArgs &p, const u64 (&S)[
 }
 
 // ---------------------------------------------------------------------------- Stage 1
-template <int NW, bool BM>
+template <int NW, bool BM, bool PACK>
 __global__ void __launch_bounds__(kBlock) k_stage1(const LaunchArgs p)
 {
     constexpr int RW = BM ? NW + 1 : NW;
@@ -395,7 +416,12 @@ __global__ void __launch_bounds__(kBlock) k_stage1(const LaunchArgs p)
                     for (int w = 0; w < NW; ++w)
                         W[w] = bit_in_word(w, x) | bit_in_word(w, u) | bit_in_word(w, y);
                 }
-                id = pack_ids(x, u, y);
+                if (PACK) {
+                    W[NW - 1] = with_packed_ids(W[NW - 1], x | (u << p.idb) | (y << (2 * p.idb)), p.idb);
+                    id = 0;
+                } else {
+                    id = pack_ids(x, u, y);
+                }
                 if (emit && p.filter)
                     emit = (shard_hash<RW>(W, id) % p.shard_count) == p.shard_index;
             }
@@ -405,31 +431,42 @@ __global__ void __launch_bounds__(kBlock) k_stage1(const LaunchArgs p)
             if (off >= p.out_cap)
                 p.sc->err = 1;
             else
-                store_record<RW>(p.pg, p.out_off + off, W, id);
+                store_record<RW, !PACK>(p.pg, p.out_off + off, W, id);
         }
     }
     flush_accum(cnt, hs, 0, p.sc);
 }
 
 // ---------------------------------------------------------------------------- Stage 2, B-mode
-// Persistent CTAs; the input tiles (kBlock*R consecutive records of one page: RW contiguous
-// word arrays + the ids array) stream into a kStages-deep shared-memory ring through TMA bulk
-// copies (cp.async.bulk + mbarrier), issued by thread 0 kStages tiles ahead of the consumers.
-constexpr int kStages = 3;
+// Persistent CTAs; the input tiles (kBlock*R consecutive records of one page: the RW contiguous
+// word arrays, plus the ids array unless ids are packed) stream into a kStages-deep shared-memory
+// ring through TMA bulk copies (cp.async.bulk + mbarrier), issued by thread 0 kStages tiles
+// ahead of the consumers.
+#ifndef CC_STAGES
+#define CC_STAGES 2
+#endif
+#ifndef CC_CHILD_CAP_X4
+#define CC_CHILD_CAP_X4 8
+#endif
+constexpr int kStages = CC_STAGES;
+constexpr int kChildCapX4 = CC_CHILD_CAP_X4;  // child list capacity = kChildCapX4/4 per path slot
 
-template <int NW>
+template <int NW, bool PACK>
 __host__ __device__ constexpr size_t blocked_stage_bytes()
 {
-    return (size_t)kBlock * expand_paths_per_thread(NW) * ((NW + 1) * 8 + 4);
+    return (size_t)kBlock * expand_paths_per_thread(NW) * ((NW + 1) * 8 + (PACK ? 0 : 4));
 }
 
-template <int NW>
+// MAXCH > 0: every path has at most MAXCH children (Delta - 1, host-checked), so the staging of
+// children is unrolled into MAXCH predicated steps instead of a divergent per-bit loop.
+template <int NW, int MAXCH, bool PACK>
 __global__ void __launch_bounds__(kBlock, NW <= 2 ? 3 : 2) k_expand_blocked(const LaunchArgs p)
 {
     constexpr int RW = NW + 1;
     constexpr int R = expand_paths_per_thread(NW);
     constexpr int kTile = kBlock * R;
-    constexpr uint32_t kStageBytes = (uint32_t)blocked_stage_bytes<NW>();
+    constexpr uint32_t kStageBytes = (uint32_t)blocked_stage_bytes<NW, PACK>();
+    constexpr uint32_t kChildCap = kChildCapX4 * kTile / 4;  // overflow falls back to per-thread appends
     extern __shared__ __align__(128) u64 smem[];
     // ring first (16-byte aligned bulk-copy destinations), then the graph tables
     char *ring = (char *)smem;
@@ -437,13 +474,14 @@ __global__ void __launch_bounds__(kBlock, NW <= 2 ? 3 : 2) k_expand_blocked(cons
     u64 *s_key = s_adj + p.g.n * NW;
     u64 *s_above = s_key + p.g.n;  // s_above[v*NW + w] = word w of {x : x > v} (the label gate)
     // staged children of one tile: parent state per path slot, one (slot, v) entry per child
-    constexpr uint32_t kChildCap = 2 * kTile;  // overflow (> 2 children per path on average) falls back
     u64 *s_par = s_above + p.g.n * NW;                    // [kTile][RW]
-    uint32_t *s_pid = (uint32_t *)(s_par + kTile * RW);   // [kTile]
-    uint32_t *s_child = s_pid + kTile;                    // [kChildCap]
+    uint32_t *s_pid = (uint32_t *)(s_par + kTile * RW);   // [kTile] (unpacked ids only)
+    uint32_t *s_child = s_pid + (PACK ? 0 : kTile);       // [kChildCap]
     __shared__ ReserveSmem rs[2];
     __shared__ __align__(8) u64 bar[kStages];
 
+    const uint32_t idb = PACK ? p.idb : (uint32_t)kIdBits;
+    const uint32_t idm = (1u << idb) - 1;
     const u64 n_tiles = (p.n_in + kTile - 1) / kTile;
     const u64 my_tiles = blockIdx.x < n_tiles ? (n_tiles - 1 - blockIdx.x) / gridDim.x + 1 : 0;
     // tile k of this CTA -> global tile blockIdx.x + k * gridDim.x -> its page and slot
@@ -459,8 +497,9 @@ __global__ void __launch_bounds__(kBlock, NW <= 2 ? 3 : 2) k_expand_blocked(cons
         for (int w = 0; w < RW; ++w)
             tma_load_1d(dst + (size_t)w * kTile * 8, pp + (((u64)w << p.pg.log_p) + slot0) * 8, kTile * 8,
                         &bar[st]);
-        tma_load_1d(dst + (size_t)RW * kTile * 8, pp + ((u64)RW << p.pg.log_p) * 8 + (u64)slot0 * 4, kTile * 4,
-                    &bar[st]);
+        if (!PACK)
+            tma_load_1d(dst + (size_t)RW * kTile * 8, pp + ((u64)RW << p.pg.log_p) * 8 + (u64)slot0 * 4,
+                        kTile * 4, &bar[st]);
     };
     if (threadIdx.x == 0) {
         for (int st = 0; st < kStages; ++st)
@@ -482,14 +521,16 @@ __global__ void __launch_bounds__(kBlock, NW <= 2 ? 3 : 2) k_expand_blocked(cons
         mbar_wait(&bar[st], (uint32_t)((k / kStages) & 1));
         const char *buf = ring + (size_t)st * kStageBytes;
         u64 W[R][RW];
-        uint32_t id[R];
+        uint32_t id[R];  // v1 | v2 << idb | vt << 2idb
+        bool valid[R];
 #pragma unroll
         for (int i = 0; i < R; ++i) {
             const int j = threadIdx.x + kBlock * i;
 #pragma unroll
             for (int w = 0; w < RW; ++w)
                 W[i][w] = ((const u64 *)buf)[w * kTile + j];
-            id[i] = base + j < p.n_in ? ((const uint32_t *)(buf + (size_t)RW * kTile * 8))[j] : 0xffffffffu;
+            valid[i] = base + j < p.n_in;
+            id[i] = PACK ? packed_ids(W[i][NW - 1], idb) : ((const uint32_t *)(buf + (size_t)RW * kTile * 8))[j];
         }
         u64 ext[R][NW];
         unsigned int ne = 0;
@@ -498,17 +539,18 @@ __global__ void __launch_bounds__(kBlock, NW <= 2 ? 3 : 2) k_expand_blocked(cons
 #pragma unroll
             for (int w = 0; w < NW; ++w)
                 ext[i][w] = 0;
-            if (id[i] == 0xffffffffu)
+            if (!valid[i])
                 continue;
-            const uint32_t v1 = id[i] & kIdMask;
-            const uint32_t v2 = (id[i] >> kIdBits) & kIdMask;
-            const uint32_t vt = id[i] >> (2 * kIdBits);
+            const uint32_t v1 = id[i] & idm;
+            const uint32_t v2 = (id[i] >> idb) & idm;
+            const uint32_t vt = id[i] >> (2 * idb);
             u64 close[NW];
             bool any_close = false;
 #pragma unroll
             for (int w = 0; w < NW; ++w) {
                 const u64 a = s_adj[vt * NW + w];
                 cand += __popcll(a);  // deg(vt): the candidate slots of Alg. 3 (statistic)
+                // the packed ids sit above bit n, where a is zero: they never leak into c
                 const u64 c = a & s_above[v2 * NW + w] & ~W[i][w];
                 const u64 a1 = s_adj[v1 * NW + w];
                 close[w] = c & a1;
@@ -543,11 +585,10 @@ __global__ void __launch_bounds__(kBlock, NW <= 2 ? 3 : 2) k_expand_blocked(cons
                 p.sc->err = 1;
         } else {
             // Staged append.  Each path with children publishes its child state (B | N[vt],
-            // keysum, v1|v2) in s_par[slot]; each child gets one 4-byte entry (slot, v) at its
-            // tile-local position in s_child.  After a barrier all threads copy the tile's
+            // keysum, and its ids) in s_par[slot]; each child gets one 4-byte entry (slot, v) at
+            // its tile-local position in s_child.  After a barrier all threads copy the tile's
             // children to their consecutive output positions: a uniform, fully coalesced loop.
-            const uint32_t loc0 = (uint32_t)(off - tile_base);
-            uint32_t loc = loc0;
+            uint32_t loc = (uint32_t)(off - tile_base);
 #pragma unroll
             for (int i = 0; i < R; ++i) {
                 bool any = false;
@@ -557,63 +598,107 @@ __global__ void __launch_bounds__(kBlock, NW <= 2 ? 3 : 2) k_expand_blocked(cons
                 if (!any)
                     continue;
                 const uint32_t slot = threadIdx.x + kBlock * i;
-                const uint32_t vt = id[i] >> (2 * kIdBits);
+                const uint32_t vt = id[i] >> (2 * idb);
 #pragma unroll
                 for (int w = 0; w < NW; ++w)
                     s_par[slot * RW + w] = W[i][w] | s_adj[vt * NW + w] | bit_in_word(w, vt);
                 s_par[slot * RW + NW] = W[i][NW];
-                s_pid[slot] = id[i] & ((1u << (2 * kIdBits)) - 1);
+                if (!PACK)
+                    s_pid[slot] = id[i] & ((1u << (2 * idb)) - 1);
+                if (MAXCH > 0) {
+                    u64 m[NW];
 #pragma unroll
-                for (int w = 0; w < NW; ++w) {
-                    u64 m = ext[i][w];
-                    while (m) {
-                        const int b = __ffsll((long long)m) - 1;
-                        m &= m - 1;
-                        if (loc < kChildCap)
-                            s_child[loc] = slot | ((uint32_t)(64 * w + b) << 16);
-                        ++loc;
+                    for (int w = 0; w < NW; ++w)
+                        m[w] = ext[i][w];
+#pragma unroll
+                    for (int c = 0; c < MAXCH; ++c) {
+                        // lowest remaining child across the words (predicated, no loop)
+                        int wsel = NW;
+#pragma unroll
+                        for (int w = NW - 1; w >= 0; --w)
+                            if (m[w])
+                                wsel = w;
+                        if (wsel < NW) {
+                            u64 x = 0;
+#pragma unroll
+                            for (int w = 0; w < NW; ++w)
+                                if (w == wsel)
+                                    x = m[w];
+                            const int b = __ffsll((long long)x) - 1;
+#pragma unroll
+                            for (int w = 0; w < NW; ++w)
+                                if (w == wsel)
+                                    m[w] = x & (x - 1);
+                            if (loc < kChildCap)
+                                s_child[loc] = slot | ((uint32_t)(64 * wsel + b) << 16);
+                            ++loc;
+                        }
+                    }
+                } else {
+#pragma unroll
+                    for (int w = 0; w < NW; ++w) {
+                        u64 m = ext[i][w];
+                        while (m) {
+                            const int b = __ffsll((long long)m) - 1;
+                            m &= m - 1;
+                            if (loc < kChildCap)
+                                s_child[loc] = slot | ((uint32_t)(64 * w + b) << 16);
+                            ++loc;
+                        }
                     }
                 }
             }
         }
         __syncthreads();
-        {
-            if (total > kChildCap) {
-                // rare (Delta > 4 with many children): fall back to per-thread appends
-                if (ne && off + ne <= p.out_cap) {
-                    Appender<RW> out;
-                    out.seek(p.pg, p.out_off + off);
+        if (total > kChildCap) {
+            // rare (many children per path): per-thread appends straight from registers
+            if (ne && off + ne <= p.out_cap) {
+                Appender<RW> out;
+                out.seek(p.pg, p.out_off + off);
 #pragma unroll
-                    for (int i = 0; i < R; ++i) {
-                        const uint32_t vt = id[i] >> (2 * kIdBits);
-                        const uint32_t v12 = id[i] & ((1u << (2 * kIdBits)) - 1);
-                        u64 C[RW];
+                for (int i = 0; i < R; ++i) {
+                    if (!valid[i])
+                        continue;
+                    const uint32_t vt = id[i] >> (2 * idb);
+                    const uint32_t v12 = id[i] & ((1u << (2 * idb)) - 1);
+                    u64 C[RW];
 #pragma unroll
-                        for (int w = 0; w < NW; ++w)
-                            C[w] = W[i][w] | s_adj[(vt & kIdMask) * NW + w] | bit_in_word(w, vt);
+                    for (int w = 0; w < NW; ++w)
+                        C[w] = W[i][w] | s_adj[vt * NW + w] | bit_in_word(w, vt);
 #pragma unroll
-                        for (int w = 0; w < NW; ++w) {
-                            u64 m = ext[i][w];
-                            while (m) {
-                                const int b = __ffsll((long long)m) - 1;
-                                m &= m - 1;
-                                const uint32_t v = (uint32_t)(64 * w + b);
-                                C[NW] = W[i][NW] + s_key[v];
-                                out.put(p.pg, C, v12 | (v << (2 * kIdBits)));
+                    for (int w = 0; w < NW; ++w) {
+                        u64 m = ext[i][w];
+                        while (m) {
+                            const int b = __ffsll((long long)m) - 1;
+                            m &= m - 1;
+                            const uint32_t v = (uint32_t)(64 * w + b);
+                            C[NW] = W[i][NW] + s_key[v];
+                            if (PACK) {
+                                C[NW - 1] = with_packed_ids(C[NW - 1], v12 | (v << (2 * idb)), idb);
+                                out.template put_words<!PACK>(p.pg, C, 0);
+                            } else {
+                                out.template put_words<!PACK>(p.pg, C, v12 | (v << (2 * idb)));
                             }
                         }
                     }
                 }
-            } else if (tile_base + total <= p.out_cap) {
-                for (unsigned int j = threadIdx.x; j < total; j += kBlock) {
-                    const uint32_t e = s_child[j];
-                    const uint32_t slot = e & 0xffffu, v = e >> 16;
-                    u64 C[RW];
+            }
+        } else if (tile_base + total <= p.out_cap) {
+            for (unsigned int j = threadIdx.x; j < total; j += kBlock) {
+                const uint32_t e = s_child[j];
+                const uint32_t slot = e & 0xffffu, v = e >> 16;
+                u64 C[RW];
 #pragma unroll
-                    for (int w = 0; w < NW; ++w)
-                        C[w] = s_par[slot * RW + w];
-                    C[NW] = s_par[slot * RW + NW] + s_key[v];
-                    store_record<RW>(p.pg, p.out_off + tile_base + j, C, s_pid[slot] | (v << (2 * kIdBits)));
+                for (int w = 0; w < NW; ++w)
+                    C[w] = s_par[slot * RW + w];
+                C[NW] = s_par[slot * RW + NW] + s_key[v];
+                if (PACK) {
+                    // child ids: (v1, v2) of the parent, last vertex v
+                    const uint32_t v12 = packed_ids(C[NW - 1], idb) & ((1u << (2 * idb)) - 1);
+                    C[NW - 1] = with_packed_ids(C[NW - 1], v12 | (v << (2 * idb)), idb);
+                    store_record<RW, false>(p.pg, p.out_off + tile_base + j, C, 0);
+                } else {
+                    store_record<RW, true>(p.pg, p.out_off + tile_base + j, C, s_pid[slot] | (v << (2 * idb)));
                 }
             }
         }
@@ -833,7 +918,7 @@ __global__ void __launch_bounds__(kBlock) k_expand_warp(const LaunchArgs p)
 }
 
 // ---------------------------------------------------------------------------- shard filter
-template <int RW>
+template <int RW, bool IDS>
 __global__ void __launch_bounds__(kBlock) k_shard_filter(const LaunchArgs p)
 {
     __shared__ ReserveSmem rs;
@@ -845,7 +930,7 @@ __global__ void __launch_bounds__(kBlock) k_shard_filter(const LaunchArgs p)
         uint32_t id = 0;
         unsigned int keep = 0;
         if (r < p.n_in) {
-            load_record<RW>(p.pg, p.pg.in_pages[base >> p.pg.log_p], (uint32_t)(r & pmask), W, id);
+            load_record<RW, IDS>(p.pg, p.pg.in_pages[base >> p.pg.log_p], (uint32_t)(r & pmask), W, id);
             keep = (shard_hash<RW>(W, id) % p.shard_count) == p.shard_index;
         }
         const u64 off = block_reserve(keep, &p.sc->out_count, rs);
@@ -853,7 +938,7 @@ __global__ void __launch_bounds__(kBlock) k_shard_filter(const LaunchArgs p)
             if (off >= p.out_cap)
                 p.sc->err = 1;
             else
-                store_record<RW>(p.pg, p.out_off + off, W, id);
+                store_record<RW, IDS>(p.pg, p.out_off + off, W, id);
         }
     }
 }
@@ -928,23 +1013,23 @@ static inline size_t graph_smem(const LaunchArgs &a)
     return ((size_t)a.g.n * (a.g.nw + 1) + kb) * sizeof(u64);
 }
 
-static size_t blocked_ring_bytes(int nw)
+static size_t blocked_ring_bytes(int nw, bool packed)
 {
     switch (nw) {
-#define RB(N) case N: return (size_t)kStages * blocked_stage_bytes<N>();
+#define RB(N) case N: return (size_t)kStages * (packed ? blocked_stage_bytes<N, true>() : blocked_stage_bytes<N, false>());
         CC_CASES(RB)
 #undef RB
     }
     return 0;
 }
 
-// dynamic shared memory of the expansion kernel for (mode, nw, n)
-size_t expand_smem(Mode m, int nw, int n)
+// dynamic shared memory of the expansion kernel for (mode, nw, n, packed)
+size_t expand_smem(Mode m, int nw, int n, bool packed)
 {
     if (m == Mode::B) {
         const size_t tile = (size_t)kBlock * expand_paths_per_thread(nw);
-        return blocked_ring_bytes(nw) + (size_t)n * (2 * nw + 1) * sizeof(u64) + tile * (nw + 1) * 8 + tile * 4 +
-               2 * tile * 4;
+        return blocked_ring_bytes(nw, packed) + (size_t)n * (2 * nw + 1) * sizeof(u64) + tile * (nw + 1) * 8 +
+               (packed ? 0 : tile * 4) + (size_t)kChildCapX4 * tile;
     }
     const size_t kb = nw <= kByteTableWords ? (size_t)8 * nw * 256 : 0;
     return ((size_t)n * (nw + 1) + kb) * sizeof(u64);
@@ -978,29 +1063,36 @@ static inline unsigned int grid_for(u64 items_per_block, u64 n, int grid_cap)
     return (unsigned int)b;
 }
 
-// kernel for (which, mode, nw); which: 0 stage1, 1 expand thread, 2 expand warp, 3 filter
-static KernelFn kernel_for(int which, Mode m, int nw)
+// kernel for (which, mode, nw, packed); which: 0 stage1, 1 expand thread, 2 expand warp,
+// 3 filter, 4 expand with at most 3 children per path
+static KernelFn kernel_for(int which, Mode m, int nw, bool pk)
 {
     const bool bm = m == Mode::B;
     switch (which) {
     case 0:
-#define K0(N) if (nw == N) return bm ? k_stage1<N, true> : k_stage1<N, false>;
+#define K0(N) if (nw == N) return bm ? (pk ? k_stage1<N, true, true> : k_stage1<N, true, false>) : k_stage1<N, false, false>;
         CC_CASES(K0)
 #undef K0
         break;
     case 1:
-#define K1(N) if (nw == N) return bm ? k_expand_blocked<N> : k_expand_thread<N>;
+    case 2:
+#define K1(N)                                                                                            \
+    if (nw == N)                                                                                         \
+        return bm ? (pk ? k_expand_blocked<N, 0, true> : k_expand_blocked<N, 0, false>)                  \
+                  : (which == 1 ? k_expand_thread<N> : k_expand_warp<N>);
         CC_CASES(K1)
 #undef K1
         break;
-    case 2:
-#define K2(N) if (nw == N) return bm ? k_expand_blocked<N> : k_expand_warp<N>;
-        CC_CASES(K2)
-#undef K2
+    case 4:
+#define K4(N)                                                                                            \
+    if (nw == N)                                                                                         \
+        return bm ? (pk ? k_expand_blocked<N, 3, true> : k_expand_blocked<N, 3, false>) : k_expand_thread<N>;
+        CC_CASES(K4)
+#undef K4
         break;
     default: {
         const int rw = record_words(nw, m);
-#define K3(N) if (rw == N) return k_shard_filter<N>;
+#define K3(N) if (rw == N) return pk ? k_shard_filter<N, false> : k_shard_filter<N, true>;
         CC_CASES(K3) K3(9)
 #undef K3
     }
@@ -1012,7 +1104,7 @@ cudaError_t launch_stage1(const LaunchArgs &a, Mode m, cudaStream_t st, int grid
 {
     if (a.n_in == 0)
         return cudaSuccess;
-    KernelFn f = kernel_for(0, m, a.g.nw);
+    KernelFn f = kernel_for(0, m, a.g.nw, a.packed != 0);
     if (!f)
         return cudaErrorInvalidValue;
     return run(f, grid_for(kBlock, a.n_in, grid_cap), graph_smem(a), st, a);
@@ -1022,8 +1114,8 @@ cudaError_t launch_expand(const LaunchArgs &a, Mode m, ExpandVariant v, cudaStre
 {
     if (a.n_in == 0)
         return cudaSuccess;
-    const int which = v == ExpandVariant::Thread ? 1 : 2;
-    KernelFn f = kernel_for(which, m, a.g.nw);
+    const int which = v == ExpandVariant::Small ? 4 : (v == ExpandVariant::Thread ? 1 : 2);
+    KernelFn f = kernel_for(which, m, a.g.nw, a.packed != 0);
     if (!f)
         return cudaErrorInvalidValue;
     u64 per_block = kBlock;
@@ -1031,14 +1123,14 @@ cudaError_t launch_expand(const LaunchArgs &a, Mode m, ExpandVariant v, cudaStre
         per_block = (u64)kBlock * expand_paths_per_thread(a.g.nw);
     else if (v == ExpandVariant::Warp)
         per_block = kBlock / 32;
-    return run(f, grid_for(per_block, a.n_in, grid_cap), expand_smem(m, a.g.nw, a.g.n), st, a);
+    return run(f, grid_for(per_block, a.n_in, grid_cap), expand_smem(m, a.g.nw, a.g.n, a.packed != 0), st, a);
 }
 
 cudaError_t launch_shard_filter(const LaunchArgs &a, Mode m, cudaStream_t st, int grid_cap)
 {
     if (a.n_in == 0)
         return cudaSuccess;
-    KernelFn f = kernel_for(3, m, a.g.nw);
+    KernelFn f = kernel_for(3, m, a.g.nw, a.packed != 0);
     if (!f)
         return cudaErrorInvalidValue;
     return run(f, grid_for(kBlock, a.n_in, grid_cap), 0, st, a);
@@ -1075,9 +1167,9 @@ cudaError_t launch_cycle_sequences(const CycleStore &c, int nw, const u64 *adj, 
     return cudaGetLastError();
 }
 
-int max_blocks_per_sm(int which, Mode m, int nw, size_t smem)
+int max_blocks_per_sm(int which, Mode m, int nw, bool packed, size_t smem)
 {
-    KernelFn f = kernel_for(which, m, nw);
+    KernelFn f = kernel_for(which, m, nw, packed);
     if (!f)
         return 1;
     const size_t sm = which == 3 ? 0 : smem;
