@@ -39,6 +39,10 @@ WORKLOADS = {
     "p8x8": (lambda: inputs.grid(8, 8), 0, "grid P8xP8 (BASELINE configs[2])"),
     "p4x4": (lambda: inputs.grid(4, 4), 0, "grid P4xP4 (BASELINE configs[0])"),
     "grid8x10": (lambda: inputs.grid(8, 10), 0, "grid P8xP10 (Table 1 row, PAPER.md:419)"),
+    "gnp2000": (lambda: inputs.gnp(2000, 0.005, inputs.GNP_SEED), 9,
+                "Erdos-Renyi G(2000, 0.005) (BASELINE configs[3]), cycles of <= 9 vertices"),
+    "gnp2000k10": (lambda: inputs.gnp(2000, 0.005, inputs.GNP_SEED), 10,
+                   "Erdos-Renyi G(2000, 0.005) (BASELINE configs[3]), cycles of <= 10 vertices"),
 }
 DEFAULT_WORKLOAD = "p10x10"
 
@@ -49,6 +53,8 @@ ORACLE_SAMPLE = {
     "p8x8": dict(),
     "p4x4": dict(),
     "grid8x10": dict(max_len=30),
+    "gnp2000": dict(max_len=8),
+    "gnp2000k10": dict(max_len=8),
 }
 
 

@@ -87,7 +87,7 @@ typedef struct {
 /* Statistics of one cc_enumerate call (cc_result_stats). */
 typedef struct {
     uint32_t struct_size;
-    uint32_t n_words;             /* 64-bit words of the path bitmap S */
+    uint32_t n_words;             /* 64-bit words per vertex bit row (S or B) */
     uint64_t total_cycles;        /* sum over k of counts[k] (counted on this shard) */
     uint64_t paths_expanded;      /* sum over t of |F_t|: paths scanned by Stage 2 */
     uint64_t candidates;          /* sum over scanned paths of deg(v_t) */
@@ -98,7 +98,7 @@ typedef struct {
     uint64_t chunks;              /* frontier chunks (== launches when nothing was split) */
     uint64_t peak_arena_records;  /* high-water mark of the frontier arena, in records */
     uint64_t arena_capacity;      /* arena capacity, in records */
-    uint64_t record_bytes;        /* bytes per frontier record (8*n_words + 4) */
+    uint64_t record_bytes;        /* bytes per frontier record */
     uint64_t bytes_alg;           /* algorithmic bytes moved by the expansion kernels
                                      (records read + records written + cycles stored) */
     uint64_t cycles_stored;       /* collect mode: cycles kept (or required, on overflow) */
@@ -135,8 +135,9 @@ cc_status cc_graph_labels(const cc_graph *g, int32_t *labels);
 
 /*
  * Enumerate every chordless cycle of g exactly once on the GPU.
- * Size classes: n <= 512 (path bitmap of <= 8 words).  Larger graphs fail with
- * CC_ERR_TOO_LARGE.  Errors: CC_ERR_NO_DEVICE, CC_ERR_CUDA, CC_ERR_CAPACITY,
+ * Size classes: n <= 512 (records of <= 8 bitmap words; count and collect mode) and
+ * 512 < n <= 2015 (wide records of <= 32 words, one warp per path; count mode only).  Larger
+ * graphs, and collect mode above n = 512, fail with CC_ERR_TOO_LARGE.  Errors: CC_ERR_NO_DEVICE, CC_ERR_CUDA, CC_ERR_CAPACITY,
  * CC_ERR_INVALID_ARGUMENT (bad options).  On success *out owns the counts, set hash,
  * per-level statistics and (collect mode) the cycles in device memory.
  */

@@ -79,7 +79,8 @@ struct cc_graph {
     std::vector<uint32_t> icol;
     std::vector<uint32_t> ifwd;
     std::vector<u64> pair_prefix;
-    int nw = 0;                     // 0 = outside the bitmap size class
+    int nw = 0;                     // words per bit row; 0 = outside every size class
+    bool wide = false;              // 512 < n <= 2015: AoS warp-per-path class (count mode only)
     std::vector<u64> adj;
     double t_build_ms = 0;
     std::mutex mu;
@@ -225,8 +226,16 @@ extern "C" cc_status cc_graph_from_csr(int64_t n, const int64_t *row_ptr, const 
         const u64 dplus = k - f;
         g->pair_prefix[i + 1] = g->pair_prefix[i] + dplus * (dplus - 1) / 2;
     }
-    if (n <= 64 * cc::kMaxWords) {
-        g->nw = n > 0 ? (int)((n + 63) / 64) : 1;
+    int wide_nw = 0;
+    if (n > 64 * cc::kMaxWords) {
+        // wide class: enough words that v1, v2, vt pack into the spare top bits
+        wide_nw = (int)((n + 3 * cc::id_bits((int)n) + 63) / 64);
+        if (wide_nw > cc::kWideMaxWords)
+            wide_nw = 0;
+    }
+    if (n <= 64 * cc::kMaxWords || wide_nw) {
+        g->nw = wide_nw ? wide_nw : (n > 0 ? (int)((n + 63) / 64) : 1);
+        g->wide = wide_nw != 0;
         g->adj.assign((size_t)n * g->nw, 0);
         for (int64_t i = 0; i < n; ++i)
             for (uint32_t k = g->irow[i]; k < g->irow[i + 1]; ++k) {
@@ -452,8 +461,10 @@ static cc_status enumerate_impl(const cc_graph *cg, const cc_options *opt_in, cc
     cc_graph *g = const_cast<cc_graph *>(cg);
     const int64_t n = g->n;
     if (n > 0 && g->nw == 0)
-        return fail(CC_ERR_TOO_LARGE, "n = " + std::to_string(n) + " exceeds the bitmap size class (n <= " +
-                                          std::to_string(64 * cc::kMaxWords) + ")");
+        return fail(CC_ERR_TOO_LARGE, "n = " + std::to_string(n) + " exceeds the supported size classes (n <= 2015)");
+    if (g->wide && opt.collect)
+        return fail(CC_ERR_TOO_LARGE, "collect mode supports n <= " + std::to_string(64 * cc::kMaxWords) +
+                                          " (n = " + std::to_string(n) + " is count mode only)");
     int ndev = 0;
     if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0)
         return fail(CC_ERR_NO_DEVICE, "no CUDA device");
@@ -500,7 +511,8 @@ static cc_status enumerate_impl(const cc_graph *cg, const cc_options *opt_in, cc
     // count mode runs on blocked-vertex records (B-mode); collect mode keeps the bitmap S
     const cc::Mode mode = opt.collect ? cc::Mode::S : cc::Mode::B;
     // B-mode records carry v1, v2, vt in the spare top bits of the blocked set when n allows
-    const bool packed = mode == cc::Mode::B && cc::packable(nw, (int)n);
+    const bool wide = g->wide;
+    const bool packed = wide || (mode == cc::Mode::B && cc::packable(nw, (int)n));
     const u64 rec_bytes = (u64)cc::record_bytes(nw, mode, packed);
     S.record_bytes = rec_bytes;
 
@@ -583,11 +595,12 @@ static cc_status enumerate_impl(const cc_graph *cg, const cc_options *opt_in, cc
                                       : g->max_deg <= 32                      ? cc::ExpandVariant::Thread
                                                                               : cc::ExpandVariant::Warp;
     const size_t gsmem = ((size_t)n * (nw + 1) + (nw <= cc::kByteTableWords ? (size_t)8 * nw * 256 : 0)) * 8;
-    const int grid_s1 = cc::max_blocks_per_sm(0, mode, nw, packed, gsmem) * sms;
+    const int grid_s1 = (wide ? cc::max_blocks_per_sm_wide(0) : cc::max_blocks_per_sm(0, mode, nw, packed, gsmem)) * sms;
     const int grid_ex =
-        cc::max_blocks_per_sm(variant == cc::ExpandVariant::Small ? 4 : variant == cc::ExpandVariant::Thread ? 1 : 2,
-                              mode, nw, packed, cc::expand_smem(mode, nw, (int)n, packed)) * sms;
-    const int grid_sf = cc::max_blocks_per_sm(3, mode, nw, packed, 0) * sms;
+        (wide ? cc::max_blocks_per_sm_wide(1)
+              : cc::max_blocks_per_sm(variant == cc::ExpandVariant::Small ? 4 : variant == cc::ExpandVariant::Thread ? 1 : 2,
+                                      mode, nw, packed, cc::expand_smem(mode, nw, (int)n, packed))) * sms;
+    const int grid_sf = (wide ? cc::max_blocks_per_sm_wide(2) : cc::max_blocks_per_sm(3, mode, nw, packed, 0)) * sms;
     const double maxfan = (double)std::max<int64_t>(g->max_deg - 1, 1);
     const uint32_t W = opt.shard_count;
     const u64 shard_threshold = (u64)(opt.min_shard_paths ? opt.min_shard_paths : 1024) * W;
@@ -642,7 +655,10 @@ static cc_status enumerate_impl(const cc_graph *cg, const cc_options *opt_in, cc
         a.filter = filter ? 1 : 0;
         if (opt.profile)
             CC_CUDA(cudaEventRecord(ea, st));
-        if (kind == STAGE1)
+        if (wide)
+            CC_CUDA(cc::launch_wide(kind == STAGE1 ? 0 : kind == EXPAND ? 1 : 2, a, st,
+                                    kind == STAGE1 ? grid_s1 : kind == EXPAND ? grid_ex : grid_sf));
+        else if (kind == STAGE1)
             CC_CUDA(cc::launch_stage1(a, mode, st, grid_s1));
         else if (kind == EXPAND)
             CC_CUDA(cc::launch_expand(a, mode, variant, st, grid_ex));

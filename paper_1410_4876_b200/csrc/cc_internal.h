@@ -130,6 +130,11 @@ cudaError_t launch_cycle_sequences(const CycleStore &c, int nw, const u64 *adj, 
                                    int32_t *out, cudaStream_t st);
 // dynamic shared memory of the expansion kernel for (mode, nw, n, packed)
 size_t expand_smem(Mode m, int nw, int n, bool packed);
+// Wide class (512 < n <= 2015, count mode, AoS records): which 0 = Stage 1, 1 = expand,
+// 2 = shard filter.
+cudaError_t launch_wide(int which, const LaunchArgs &a, cudaStream_t st, int grid_cap);
+int max_blocks_per_sm_wide(int which);
+constexpr int kWideMaxWords = 32;
 // Resident CTAs per SM at kBlock threads with the given dynamic smem.
 // which: 0 = Stage 1, 1 = expand (thread), 2 = expand (warp), 3 = shard filter, 4 = expand (small)
 int max_blocks_per_sm(int which, Mode m, int nw, bool packed, size_t smem);

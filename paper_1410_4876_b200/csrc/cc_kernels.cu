@@ -90,14 +90,19 @@ __device__ __forceinline__ void store_record(const Pages &pg, u64 o, const u64 (
 }
 
 // Packed B-mode ids: v1 | v2 << idb | vt << 2idb in the top 3*idb bits of word NW-1.
-__device__ __forceinline__ uint32_t packed_ids(u64 last_word, uint32_t idb)
+// (3*idb can exceed 32 bits: idb = 11 for n = 2000, so the packed ids are 64-bit values)
+__device__ __forceinline__ u64 packed_ids(u64 last_word, uint32_t idb)
 {
-    return (uint32_t)(last_word >> (64 - 3 * idb));
+    return last_word >> (64 - 3 * idb);
 }
-__device__ __forceinline__ u64 with_packed_ids(u64 last_word, uint32_t ids, uint32_t idb)
+__device__ __forceinline__ u64 with_packed_ids(u64 last_word, u64 ids, uint32_t idb)
 {
     const u64 low = (1ull << (64 - 3 * idb)) - 1;
-    return (last_word & low) | ((u64)ids << (64 - 3 * idb));
+    return (last_word & low) | (ids << (64 - 3 * idb));
+}
+__device__ __forceinline__ u64 pack3(uint32_t a, uint32_t b, uint32_t c, uint32_t idb)
+{
+    return (u64)a | ((u64)b << idb) | ((u64)c << (2 * idb));
 }
 
 template <int RW>
@@ -417,7 +422,7 @@ __global__ void __launch_bounds__(kBlock) k_stage1(const LaunchArgs p)
                         W[w] = bit_in_word(w, x) | bit_in_word(w, u) | bit_in_word(w, y);
                 }
                 if (PACK) {
-                    W[NW - 1] = with_packed_ids(W[NW - 1], x | (u << p.idb) | (y << (2 * p.idb)), p.idb);
+                    W[NW - 1] = with_packed_ids(W[NW - 1], pack3(x, u, y, p.idb), p.idb);
                     id = 0;
                 } else {
                     id = pack_ids(x, u, y);
@@ -943,6 +948,220 @@ __global__ void __launch_bounds__(kBlock) k_shard_filter(const LaunchArgs p)
     }
 }
 
+// ---------------------------------------------------------------------------- wide class
+// Graphs with 512 < n <= 2015 (e.g. G(2000, 0.005), BASELINE configs[3]).  Count mode only.
+// Records are array-of-structures, RW = NW + 1 words each: the blocked set B(p) in words
+// 0..NW-1 (v1, v2, vt packed in the top 3*idb bits of word NW-1; NW is chosen so those bits
+// are free) and keysum(p) in word NW.  One warp handles one path: lane w owns word w (NW <= 32),
+// so a record is read and written as one coalesced 8*RW-byte line.  Adjacency rows (n*NW
+// words, ~0.5 MB) are read through L1/L2 instead of shared memory.
+__device__ __forceinline__ u64 *wide_rec(const Pages &pg, const uint32_t *pages, u64 r, int RW)
+{
+    return (u64 *)(pg.base + (u64)pages[r >> pg.log_p] * pg.page_bytes) +
+           (r & ((1ull << pg.log_p) - 1)) * (u64)RW;
+}
+
+__device__ __forceinline__ u64 above_word(uint32_t v2, int w)
+{
+    const int sh = (int)v2 + 1 - 64 * w;
+    return sh <= 0 ? ~0ull : (sh >= 64 ? 0ull : (~0ull << sh));
+}
+
+__global__ void __launch_bounds__(kBlock) k_stage1_wide(const LaunchArgs p)
+{
+    __shared__ ReserveSmem rs;
+    const int n = p.g.n, NW = p.g.nw, RW = NW + 1;
+    const u64 *__restrict__ adj = p.g.adj;
+    const u64 *__restrict__ key = p.g.key;
+    u64 cnt = 0, hs = 0;
+    const u64 stride = (u64)gridDim.x * kBlock;
+    for (u64 base = (u64)blockIdx.x * kBlock; base < p.n_in; base += stride) {
+        const u64 r = base + threadIdx.x;
+        unsigned int emit = 0;
+        uint32_t x = 0, u = 0, y = 0;
+        u64 h = 0;
+        if (r < p.n_in) {
+            const u64 gid = p.in_lo + r;
+            int lo = 0, hi = n - 1;
+            while (lo < hi) {
+                const int mid = (lo + hi + 1) >> 1;
+                if (p.g.pair_prefix[mid] <= gid)
+                    lo = mid;
+                else
+                    hi = mid - 1;
+            }
+            u = (uint32_t)lo;
+            const u64 q = gid - p.g.pair_prefix[u];
+            u64 j = (u64)((1.0 + sqrt(1.0 + 8.0 * (double)q)) * 0.5);
+            while (j * (j - 1) / 2 > q)
+                --j;
+            while ((j + 1) * j / 2 <= q)
+                ++j;
+            const u64 i = q - j * (j - 1) / 2;
+            const uint32_t f = p.g.fwd[u];
+            x = p.g.col[f + (uint32_t)i];
+            y = p.g.col[f + (uint32_t)j];
+            const bool tri = (__ldg(adj + (u64)x * NW + (y >> 6)) >> (y & 63)) & 1ull;
+            if (tri) {
+                if (p.count) {
+                    cnt++;
+                    hs += mix64(__ldg(key + x) + __ldg(key + u) + __ldg(key + y));
+                }
+            } else if (p.emit) {
+                emit = 1;
+                if (p.root_stride > 1) {
+                    const u64 rkey = ((u64)p.g.orig[x] << 42) | ((u64)p.g.orig[u] << 21) | (u64)p.g.orig[y];
+                    emit = (mix64(rkey) % p.root_stride) == p.root_offset;
+                }
+                if (emit && p.filter) {  // shard hash over the record words, as k_shard_filter_wide
+                    h = mix64(0ull);
+                    for (int w = 0; w < NW; ++w) {
+                        u64 word = __ldg(adj + (u64)u * NW + w) | bit_in_word(w, u);
+                        if (w == NW - 1)
+                            word = with_packed_ids(word, pack3(x, u, y, p.idb), p.idb);
+                        h = mix64(h ^ word);
+                    }
+                    h = mix64(h ^ (__ldg(key + x) + __ldg(key + u) + __ldg(key + y)));
+                    emit = (h % p.shard_count) == p.shard_index;
+                }
+            }
+        }
+        const u64 off = block_reserve(emit, &p.sc->out_count, rs);
+        if (emit) {
+            if (off >= p.out_cap) {
+                p.sc->err = 1;
+            } else {
+                u64 *rec = wide_rec(p.pg, p.pg.out_pages, p.out_off + off, RW);
+                for (int w = 0; w < NW; ++w) {  // B(<x,u,y>) = N[u]
+                    u64 word = __ldg(adj + (u64)u * NW + w) | bit_in_word(w, u);
+                    if (w == NW - 1)
+                        word = with_packed_ids(word, pack3(x, u, y, p.idb), p.idb);
+                    rec[w] = word;
+                }
+                rec[NW] = __ldg(key + x) + __ldg(key + u) + __ldg(key + y);
+            }
+        }
+    }
+    flush_accum(cnt, hs, 0, p.sc);
+}
+
+constexpr int kWidePaths = 4;  // paths per warp per tile in k_expand_wide
+
+__global__ void __launch_bounds__(kBlock) k_expand_wide(const LaunchArgs p)
+{
+    __shared__ ReserveSmem rs;
+    const int NW = p.g.nw, RW = NW + 1;
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    const uint32_t idb = p.idb, idm = (1u << idb) - 1;
+    const u64 *__restrict__ adj = p.g.adj;
+    const u64 *__restrict__ key = p.g.key;
+    const bool mine = lane < NW;  // this lane owns word `lane` of every record
+    constexpr u64 kTilePaths = (u64)(kBlock / 32) * kWidePaths;
+    u64 cnt = 0, hs = 0, cand = 0;
+    for (u64 tb = (u64)blockIdx.x * kTilePaths; tb < p.n_in; tb += (u64)gridDim.x * kTilePaths) {
+        u64 ext[kWidePaths], Cw[kWidePaths], ksv[kWidePaths];
+        u64 v12v[kWidePaths];
+        unsigned int ne = 0;
+#pragma unroll
+        for (int i = 0; i < kWidePaths; ++i) {
+            ext[i] = 0;
+            Cw[i] = 0;
+            ksv[i] = 0;
+            v12v[i] = 0;
+            const u64 r = tb + (u64)wid * kWidePaths + i;
+            if (r >= p.n_in)
+                continue;  // warp-uniform
+            const u64 *rec = wide_rec(p.pg, p.pg.in_pages, r, RW);
+            const u64 B = mine ? rec[lane] : 0ull;
+            const u64 ks = __shfl_sync(FULL_MASK, lane == 0 ? rec[NW] : 0ull, 0);
+            const u64 id = packed_ids(__shfl_sync(FULL_MASK, B, NW - 1), idb);
+            const uint32_t v1 = (uint32_t)(id & idm), v2 = (uint32_t)((id >> idb) & idm),
+                           vt = (uint32_t)(id >> (2 * idb));
+            const u64 a = mine ? __ldg(adj + (u64)vt * NW + lane) : 0ull;
+            const u64 a1 = mine ? __ldg(adj + (u64)v1 * NW + lane) : 0ull;
+            const u64 c = a & above_word(v2, lane) & ~B;
+            u64 close = c & a1;
+            ext[i] = p.emit ? (c & ~a1) : 0ull;
+            if (p.count) {
+                cand += __popcll(a);
+                cnt += __popcll(close);
+                while (close) {
+                    const int b = __ffsll((long long)close) - 1;
+                    close &= close - 1;
+                    hs += mix64(ks + __ldg(key + 64 * lane + b));
+                }
+            }
+            ne += __reduce_add_sync(FULL_MASK, (unsigned int)__popcll(ext[i]));
+            // the children's blocked set: vt becomes interior -> B | N[vt]
+            Cw[i] = mine ? (B | a | bit_in_word(lane, vt)) : 0ull;
+            ksv[i] = ks;
+            v12v[i] = id & ((1ull << (2 * idb)) - 1);
+        }
+        // one reservation per CTA tile; the warp's count is carried by its lane 0
+        const u64 off = __shfl_sync(FULL_MASK, block_reserve(lane == 0 ? ne : 0u, &p.sc->out_count, rs), 0);
+        if (ne == 0)
+            continue;
+        if (off + ne > p.out_cap) {
+            if (lane == 0)
+                p.sc->err = 1;
+            continue;
+        }
+        u64 o = p.out_off + off;
+#pragma unroll
+        for (int i = 0; i < kWidePaths; ++i) {
+            u64 m = ext[i];
+            for (;;) {
+                const unsigned int has = __ballot_sync(FULL_MASK, m != 0ull);
+                if (!has)
+                    break;
+                const int L = __ffs(has) - 1;  // lowest word with a child
+                const int b = __shfl_sync(FULL_MASK, __ffsll((long long)m) - 1, L);
+                if (lane == L)
+                    m &= m - 1;
+                const uint32_t v = (uint32_t)(64 * L + b);
+                u64 *rec = wide_rec(p.pg, p.pg.out_pages, o, RW);
+                if (mine)
+                    rec[lane] = lane == NW - 1 ? with_packed_ids(Cw[i], v12v[i] | ((u64)v << (2 * idb)), idb) : Cw[i];
+                if (lane == 0)
+                    rec[NW] = ksv[i] + __ldg(key + v);
+                ++o;
+            }
+        }
+    }
+    if (!p.count)
+        cand = 0;
+    flush_accum(cnt, hs, cand, p.sc);
+}
+
+__global__ void __launch_bounds__(kBlock) k_shard_filter_wide(const LaunchArgs p)
+{
+    __shared__ ReserveSmem rs;
+    const int NW = p.g.nw, RW = NW + 1;
+    const u64 stride = (u64)gridDim.x * kBlock;
+    for (u64 base = (u64)blockIdx.x * kBlock; base < p.n_in; base += stride) {
+        const u64 r = base + threadIdx.x;
+        unsigned int keep = 0;
+        const u64 *src = nullptr;
+        if (r < p.n_in) {
+            src = wide_rec(p.pg, p.pg.in_pages, r, RW);
+            u64 h = mix64(0ull);
+            for (int w = 0; w < RW; ++w)
+                h = mix64(h ^ src[w]);
+            keep = (h % p.shard_count) == p.shard_index;
+        }
+        const u64 off = block_reserve(keep, &p.sc->out_count, rs);
+        if (keep) {
+            if (off >= p.out_cap) {
+                p.sc->err = 1;
+            } else {
+                u64 *dst = wide_rec(p.pg, p.pg.out_pages, p.out_off + off, RW);
+                for (int w = 0; w < RW; ++w)
+                    dst[w] = src[w];
+            }
+        }
+    }
+}
+
 // ---------------------------------------------------------------------------- keys, collect
 __global__ void k_keys(u64 *key, const int32_t *orig, int n, u64 seed)
 {
@@ -1098,6 +1317,24 @@ static KernelFn kernel_for(int which, Mode m, int nw, bool pk)
     }
     }
     return nullptr;
+}
+
+cudaError_t launch_wide(int which, const LaunchArgs &a, cudaStream_t st, int grid_cap)
+{
+    if (a.n_in == 0)
+        return cudaSuccess;
+    KernelFn f = which == 0 ? k_stage1_wide : which == 1 ? k_expand_wide : k_shard_filter_wide;
+    const u64 per_block = which == 1 ? (u64)(kBlock / 32) * kWidePaths : (u64)kBlock;
+    return run(f, grid_for(per_block, a.n_in, grid_cap), 0, st, a);
+}
+
+int max_blocks_per_sm_wide(int which)
+{
+    KernelFn f = which == 0 ? k_stage1_wide : which == 1 ? k_expand_wide : k_shard_filter_wide;
+    int nb = 1;
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, (const void *)f, kBlock, 0) != cudaSuccess || nb < 1)
+        nb = 1;
+    return nb;
 }
 
 cudaError_t launch_stage1(const LaunchArgs &a, Mode m, cudaStream_t st, int grid_cap)

@@ -231,10 +231,59 @@ def test_unsorted_rows_and_permuted_ids(ws):
 
 
 def test_too_large_graph_rejected(ws):
-    g = I.gnp(600, 0.01, 1)
+    g = I.gnp(2016, 0.002, 1)
     with pytest.raises(binding.CCError) as ei:
         gpu(g, ws)
     assert ei.value.kind == "CC_ERR_TOO_LARGE"
+    # collect mode is limited to the bitmap class n <= 512
+    with pytest.raises(binding.CCError) as ei:
+        gpu(I.gnp(600, 0.005, 1), ws, collect=True)
+    assert ei.value.kind == "CC_ERR_TOO_LARGE"
+
+
+# ---------------------------------------------------------------- wide class (512 < n <= 2015)
+@pytest.mark.parametrize("K", [3, 4, 5, 6, 7, 8])
+def test_gnp2000_config3_capped(ws, K):
+    """BASELINE configs[3]: G(2000, 0.005) (seed inputs.GNP_SEED) per-length counts + set hash
+    with a length cap (full enumeration is infeasible: ~1e190 cycles)."""
+    g = I.gnp(2000, 0.005, I.GNP_SEED)
+    assert_same(gpu(g, ws, max_len=K), oracle.enumerate_cycles(*g, max_len=K, nthreads=NT))
+
+
+@pytest.mark.parametrize("n,p,K", [(513, 0.02, 7), (600, 0.01, 9), (1024, 0.006, 8), (1500, 0.004, 9),
+                                   (2015, 0.003, 9)])
+def test_wide_class_sizes(ws, n, p, K):
+    g = I.gnp(n, p, 4000 + n)
+    assert_same(gpu(g, ws, max_len=K), oracle.enumerate_cycles(*g, max_len=K, nthreads=NT))
+
+
+def test_wide_class_dense_and_grid(ws):
+    """Wide class on a denser random graph (closures every level) and on a long-path graph."""
+    g = I.gnp(700, 0.05, 9)
+    assert_same(gpu(g, ws, max_len=5), oracle.enumerate_cycles(*g, max_len=5, nthreads=NT))
+    g = I.grid(24, 24)  # n = 576, long chordless paths
+    assert_same(gpu(g, ws, max_len=16), oracle.enumerate_cycles(*g, max_len=16, nthreads=NT))
+
+
+@pytest.mark.parametrize("W", [2, 5])
+def test_wide_class_shards(ws, W):
+    g = I.gnp(2000, 0.005, I.GNP_SEED)
+    full = gpu(g, ws, max_len=7)
+    parts = [gpu(g, ws, max_len=7, shard_index=i, shard_count=W) for i in range(W)]
+    assert sum(p["counts"] for p in parts).tolist() == full["counts"].tolist()
+    assert sum(p["set_hash"] for p in parts) % (1 << 64) == full["set_hash"]
+    assert sum(p["paths_by_len"] for p in parts).tolist() == full["paths_by_len"].tolist()
+
+
+def test_wide_class_chunked(ws):
+    import torch
+    g = I.gnp(2000, 0.005, I.GNP_SEED)
+    # 256 pages of 1024 records (~69 MB) cannot hold the ~12 M-path F_6, so levels are split; a page
+    # must still fit one page of children (fan-out up to ~8 here), see DESIGN.md §5
+    small = torch.empty(256 * 1024 * 264, dtype=torch.uint8, device="cuda")
+    got = binding.enumerate_cycles(*g, workspace=small, max_len=7)
+    assert got["stats"]["chunks"] > got["stats"]["rounds"]
+    assert_same(got, oracle.enumerate_cycles(*g, max_len=7, nthreads=NT))
 
 
 def test_repeat_runs_deterministic(ws):
