@@ -48,7 +48,7 @@ DEFAULT_WORKLOAD = "p10x10"
 
 # oracle samples (bounded CPU work, ~10-30 s) for cpu_baseline / --impl reference
 ORACLE_SAMPLE = {
-    "p10x10": dict(max_len=26),
+    "p10x10": dict(max_len=31),
     "k150": dict(),
     "p8x8": dict(),
     "p4x4": dict(),
@@ -196,10 +196,18 @@ def main():
     from paper_1410_4876_b200 import binding
 
     rank, world, local = dist_env()
+    # one process per GPU; CC_DIST_BACKEND=gloo (+ several ranks per GPU) is only for checking
+    # the N > 1 path on a one-GPU box
+    backend = os.environ.get("CC_DIST_BACKEND", "nccl")
+    local = local % max(torch.cuda.device_count(), 1)
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     if world > 1:
-        dist.init_process_group("nccl", device_id=dev)
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=dev)
+        else:
+            dist.init_process_group(backend)
+    comm_dev = dev if backend == "nccl" else None
     stream = torch.cuda.current_stream()
     sh = stream.cuda_stream
 
@@ -248,8 +256,8 @@ def main():
     paths_local = int(paths.sum())
     if world > 1:
         from paper_1410_4876_b200 import dist as D
-        dev_ms = D.max_over_ranks(dev_ms, device=dev)
-        counts, h, paths_total = D.combine_shards(counts, h, paths_local, device=dev)
+        dev_ms = D.max_over_ranks(dev_ms, device=comm_dev)
+        counts, h, paths_total = D.combine_shards(counts, h, paths_local, device=comm_dev)
     else:
         paths_total = paths_local
     cycles_total = int(counts.sum())
@@ -273,7 +281,7 @@ def main():
             traffic = None
     roofline = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                 "frac": achieved / peak, "traffic": traffic, "peak_kind": peak_kind,
-                "kernel": "k_expand_thread/k_expand_warp", "expand_share_of_step": t_expand / dev_ms if dev_ms else None,
+                "kernel": "k_expand_blocked" if g[0] <= 512 else "k_expand_wide", "expand_share_of_step": t_expand / dev_ms if dev_ms else None,
                 "bytes_alg_per_step": bytes_alg / args.steps}
 
     # ---- end to end through the public API with host buffers (labelling + upload + D2H)
@@ -298,7 +306,7 @@ def main():
         el = time.perf_counter() - t0
         if world > 1:
             from paper_1410_4876_b200 import dist as D
-            el = D.max_over_ranks(el, device=dev)
+            el = D.max_over_ranks(el, device=comm_dev)
         e2e = {"value": cycles_total / (el / ne), "unit": UNIT, "h2d_bytes_per_step": h2d // ne,
                "d2h_bytes_per_step": d2h // ne, "ms_per_step": 1e3 * el / ne}
 

@@ -18,6 +18,7 @@
 
 #include <algorithm>
 #include <chrono>
+#include <cmath>
 #include <cstddef>
 #include <cstdio>
 #include <cstdlib>
@@ -767,7 +768,11 @@ static cc_status enumerate_impl(const cc_graph *cg, const cc_options *opt_in, cc
         if (emit && (W == 1 || L.sharded)) {
             double f = L.fan > 0 ? L.fan * 1.15 : (levels[d - 1].fan > 0 ? levels[d - 1].fan * 1.5 : maxfan);
             f = std::min(std::max(f, 0.05), maxfan);
-            const double room = (double)free_pages.size() * P;
+            // keep a reserve so that the child level can expand its first page next (about
+            // f pages of grandchildren): without it a high fan-out level fills every free page
+            // with children that then cannot be expanded
+            const double reserve = (std::ceil(f * 1.2) + 1.0) * (double)P;
+            const double room = std::max((double)P, (double)free_pages.size() * P - reserve);
             // records of the last k pages: (k-1) full pages + the partial last page
             const u64 last_fill = L.count - (u64)(L.pages.size() - 1) * P;
             u64 take = (u64)std::max(1.0, room / f);
