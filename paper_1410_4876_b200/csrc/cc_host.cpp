@@ -630,7 +630,23 @@ static cc_status enumerate_impl(const cc_graph *cg, const cc_options *opt_in, cc
     // free pages; on success the used output pages are returned in `used` and the scratch
     // in *h_sc.  Returns CC_OK, or CC_ERR_CAPACITY with *overflow set when the output did not
     // fit (nothing is committed: the caller retries with less input).
+    // Optional per-launch trace (env CC_TRACE=<file>): one CSV line per kernel launch -- the
+    // evolution of |T| and |C| per step that the paper plots in Fig. 4.
+    struct TraceFile {
+        FILE *f = nullptr;
+        ~TraceFile()
+        {
+            if (f)
+                fclose(f);
+        }
+    } trace;
+    if (const char *tp = std::getenv("CC_TRACE")) {
+        trace.f = std::fopen(tp, "a");
+        if (trace.f)
+            std::fprintf(trace.f, "kind,level,paths_in,children_out,cycles,candidates,ms,overflow\n");
+    }
     enum Kind { STAGE1, EXPAND, FILTER };
+    int trace_level = 0;
     auto launch = [&](Kind kind, const uint32_t *in, size_t n_in_pages, u64 n_in, u64 pair_lo, bool emit,
                       bool count, bool filter, std::vector<uint32_t> &used, bool *overflow) -> cc_status {
         *overflow = false;
@@ -671,14 +687,20 @@ static cc_status enumerate_impl(const cc_graph *cg, const cc_options *opt_in, cc
         CC_CUDA(cudaStreamSynchronize(st));
         S.d2h_bytes += sizeof(cc::Scratch);
         S.launches++;
+        float ms = 0;
         if (opt.profile) {
-            float ms = 0;
             CC_CUDA(cudaEventElapsedTime(&ms, ea, eb));
             if (kind == STAGE1)
                 S.t_stage1_ms += ms;
             else if (kind == EXPAND)
                 S.t_expand_ms += ms;
         }
+        if (trace.f)
+            std::fprintf(trace.f, "%s,%d,%llu,%llu,%llu,%llu,%.6f,%d\n",
+                         kind == STAGE1 ? "stage1" : kind == EXPAND ? "expand" : "filter", trace_level,
+                         (unsigned long long)n_in, (unsigned long long)h_sc->out_count,
+                         (unsigned long long)h_sc->cycles, (unsigned long long)h_sc->cand, ms,
+                         (h_sc->err || h_sc->out_count > a.out_cap) ? 1 : 0);
         if (h_sc->err || h_sc->out_count > a.out_cap) {
             *overflow = true;
             if (opt.collect) {  // roll back the cycles this launch stored
@@ -720,6 +742,7 @@ static cc_status enumerate_impl(const cc_graph *cg, const cc_options *opt_in, cc
             if (c == 0)
                 return fail(CC_ERR_CAPACITY, "no free arena page for Stage 1");
             bool of = false;
+            trace_level = 2;
             cc_status s = launch(STAGE1, nullptr, 0, c, s1_next, want_paths, count_tri, s1_filter, used, &of);
             if (s != CC_OK)
                 return s;
@@ -742,6 +765,7 @@ static cc_status enumerate_impl(const cc_graph *cg, const cc_options *opt_in, cc
         // ---- multi-GPU: partition the first frontier level with >= threshold paths
         if (W > 1 && !L.sharded && L.count >= shard_threshold) {
             bool of = false;
+            trace_level = d;
             cc_status s = launch(FILTER, L.pages.data(), L.pages.size(), L.count, 0, true, false, false, used, &of);
             if (s != CC_OK)
                 return s;
@@ -788,6 +812,7 @@ static cc_status enumerate_impl(const cc_graph *cg, const cc_options *opt_in, cc
             const u64 c = last_fill + (u64)(k - 1) * P;
             const uint32_t *in = L.pages.data() + (L.pages.size() - k);
             bool of = false;
+            trace_level = d;
             cc_status s = launch(EXPAND, in, k, c, 0, emit, owner, false, used, &of);
             if (s != CC_OK)
                 return s;

@@ -81,10 +81,11 @@ __device__ __forceinline__ void store_record(const Pages &pg, u64 o, const u64 (
     const uint32_t page = pg.out_pages[o >> pg.log_p];
     const uint32_t slot = (uint32_t)(o & ((1ull << pg.log_p) - 1));
     char *pp = page_ptr(pg, page);
-    u64 *w = (u64 *)pp;
+    u64 *w0 = (u64 *)pp + slot;
+    const u64 pw = 1ull << pg.log_p;  // words between consecutive word arrays
 #pragma unroll
     for (int k = 0; k < RW; ++k)
-        w[((u64)k << pg.log_p) + slot] = W[k];
+        w0[k * pw] = W[k];
     if (IDS)
         ((uint32_t *)(pp + ((u64)RW << pg.log_p) * 8))[slot] = id;
 }
@@ -157,6 +158,46 @@ __device__ __forceinline__ u64 block_reserve2(unsigned int c, u64 *counter, Rese
     __syncthreads();
     return sm.base + sm.warp[wid] + (incl - c);
 }
+
+// Split reservation.  reserve_begin: block scan (2 barriers) -> this thread's TILE-LOCAL offset;
+// the last lane of warp 0 issues the global atomicAdd and keeps its (in-flight) result in
+// *ticket.  That lane calls reserve_publish(ticket) later, after independent work, so the
+// atomic's round trip overlaps that work instead of stalling every warp at a barrier; the base
+// is visible to all threads after the caller's next barrier.
+__device__ __forceinline__ unsigned int reserve_begin(unsigned int c, u64 *counter, ReserveSmem &sm, u64 *ticket)
+{
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    unsigned int incl = c;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const unsigned int v = __shfl_up_sync(FULL_MASK, incl, o);
+        if (lane >= o)
+            incl += v;
+    }
+    if (lane == 31)
+        sm.warp[wid] = incl;
+    __syncthreads();
+    if (wid == 0) {
+        const unsigned int w = lane < kBlock / 32 ? sm.warp[lane] : 0u;
+        unsigned int wi = w;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const unsigned int v = __shfl_up_sync(FULL_MASK, wi, o);
+            if (lane >= o)
+                wi += v;
+        }
+        if (lane < kBlock / 32)
+            sm.warp[lane] = wi - w;
+        if (lane == kBlock / 32 - 1) {
+            sm.total = wi;
+            *ticket = wi ? atomicAdd(counter, (u64)wi) : 0ull;
+        }
+    }
+    __syncthreads();
+    return sm.warp[wid] + (incl - c);
+}
+
+__device__ __forceinline__ bool is_ticket_lane() { return threadIdx.x == kBlock / 32 - 1; }
 
 // single-buffer form: a third barrier protects sm before its next use
 __device__ __forceinline__ u64 block_reserve(unsigned int c, u64 *counter, ReserveSmem &sm)
@@ -479,8 +520,9 @@ __global__ void __launch_bounds__(kBlock, NW <= 2 ? 3 : 2) k_expand_blocked(cons
     u64 *s_key = s_adj + p.g.n * NW;
     u64 *s_above = s_key + p.g.n;  // s_above[v*NW + w] = word w of {x : x > v} (the label gate)
     // staged children of one tile: parent state per path slot, one (slot, v) entry per child
-    u64 *s_par = s_above + p.g.n * NW;                    // [kTile][RW]
-    uint32_t *s_pid = (uint32_t *)(s_par + kTile * RW);   // [kTile] (unpacked ids only)
+    constexpr int PW = RW + NW;                           // parent child state + extension words
+    u64 *s_par = s_above + p.g.n * NW;                    // [kTile][PW]
+    uint32_t *s_pid = (uint32_t *)(s_par + kTile * PW);   // [kTile] (unpacked ids only)
     uint32_t *s_child = s_pid + (PACK ? 0 : kTile);       // [kChildCap]
     __shared__ ReserveSmem rs[2];
     __shared__ __align__(8) u64 bar[kStages];
@@ -577,23 +619,20 @@ __global__ void __launch_bounds__(kBlock, NW <= 2 ? 3 : 2) k_expand_blocked(cons
                 }
             }
         }
-        // every thread has read stage st (block_reserve starts with a barrier) -> refill it
-        const u64 off = block_reserve2(ne, &p.sc->out_count, rs[k & 1]);
+        // every thread has read stage st (the reservation starts with a barrier) -> refill it
+        u64 ticket = 0;
+        const unsigned int loc0 = reserve_begin(ne, &p.sc->out_count, rs[k & 1], &ticket);
         if (threadIdx.x == 0 && k + kStages < my_tiles) {
             asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
             issue(k + kStages);
         }
-        const u64 tile_base = rs[k & 1].base;  // first output position of this CTA tile
         const unsigned int total = rs[k & 1].total;
-        if (off + ne > p.out_cap) {
-            if (ne)
-                p.sc->err = 1;
-        } else {
+        {
             // Staged append.  Each path with children publishes its child state (B | N[vt],
             // keysum, and its ids) in s_par[slot]; each child gets one 4-byte entry (slot, v) at
             // its tile-local position in s_child.  After a barrier all threads copy the tile's
             // children to their consecutive output positions: a uniform, fully coalesced loop.
-            uint32_t loc = (uint32_t)(off - tile_base);
+            uint32_t loc = loc0;
 #pragma unroll
             for (int i = 0; i < R; ++i) {
                 bool any = false;
@@ -606,39 +645,24 @@ __global__ void __launch_bounds__(kBlock, NW <= 2 ? 3 : 2) k_expand_blocked(cons
                 const uint32_t vt = id[i] >> (2 * idb);
 #pragma unroll
                 for (int w = 0; w < NW; ++w)
-                    s_par[slot * RW + w] = W[i][w] | s_adj[vt * NW + w] | bit_in_word(w, vt);
-                s_par[slot * RW + NW] = W[i][NW];
+                    s_par[slot * PW + w] = W[i][w] | s_adj[vt * NW + w] | bit_in_word(w, vt);
+                s_par[slot * PW + NW] = W[i][NW];
                 if (!PACK)
                     s_pid[slot] = id[i] & ((1u << (2 * idb)) - 1);
                 if (MAXCH > 0) {
-                    u64 m[NW];
+                    // entries (slot, rank): the copy phase finds the rank-th child itself
 #pragma unroll
                     for (int w = 0; w < NW; ++w)
-                        m[w] = ext[i][w];
+                        s_par[slot * PW + RW + w] = ext[i][w];
+                    uint32_t nc = 0;
 #pragma unroll
-                    for (int c = 0; c < MAXCH; ++c) {
-                        // lowest remaining child across the words (predicated, no loop)
-                        int wsel = NW;
+                    for (int w = 0; w < NW; ++w)
+                        nc += __popcll(ext[i][w]);
 #pragma unroll
-                        for (int w = NW - 1; w >= 0; --w)
-                            if (m[w])
-                                wsel = w;
-                        if (wsel < NW) {
-                            u64 x = 0;
-#pragma unroll
-                            for (int w = 0; w < NW; ++w)
-                                if (w == wsel)
-                                    x = m[w];
-                            const int b = __ffsll((long long)x) - 1;
-#pragma unroll
-                            for (int w = 0; w < NW; ++w)
-                                if (w == wsel)
-                                    m[w] = x & (x - 1);
-                            if (loc < kChildCap)
-                                s_child[loc] = slot | ((uint32_t)(64 * wsel + b) << 16);
-                            ++loc;
-                        }
-                    }
+                    for (int c = 0; c < MAXCH; ++c)
+                        if ((uint32_t)c < nc && loc + c < kChildCap)
+                            s_child[loc + c] = slot | ((uint32_t)c << 16);
+                    loc += nc;
                 } else {
 #pragma unroll
                     for (int w = 0; w < NW; ++w) {
@@ -654,7 +678,13 @@ __global__ void __launch_bounds__(kBlock, NW <= 2 ? 3 : 2) k_expand_blocked(cons
                 }
             }
         }
+        if (is_ticket_lane())
+            rs[k & 1].base = ticket;  // the atomic's result is needed only now
         __syncthreads();
+        const u64 tile_base = rs[k & 1].base;  // first output position of this CTA tile
+        const u64 off = tile_base + loc0;
+        if (ne && off + ne > p.out_cap)
+            p.sc->err = 1;
         if (total > kChildCap) {
             // rare (many children per path): per-thread appends straight from registers
             if (ne && off + ne <= p.out_cap) {
@@ -691,12 +721,37 @@ __global__ void __launch_bounds__(kBlock, NW <= 2 ? 3 : 2) k_expand_blocked(cons
         } else if (tile_base + total <= p.out_cap) {
             for (unsigned int j = threadIdx.x; j < total; j += kBlock) {
                 const uint32_t e = s_child[j];
-                const uint32_t slot = e & 0xffffu, v = e >> 16;
+                const uint32_t slot = e & 0xffffu;
+                uint32_t v;
+                if (MAXCH > 0) {
+                    // v = the rank-th (rank < MAXCH) set bit of the parent's extension words:
+                    // pick the word by popcount, drop `rank` low bits (selects), find-first-set
+                    uint32_t r = e >> 16;
+                    u64 x = s_par[slot * PW + RW];
+                    uint32_t wsel = 0;
+#pragma unroll
+                    for (int w = 1; w < NW; ++w) {
+                        const uint32_t pc = __popcll(x);
+                        const u64 nx = s_par[slot * PW + RW + w];
+                        const bool next = r >= pc;
+                        r = next ? r - pc : r;
+                        wsel = next ? (uint32_t)w : wsel;
+                        x = next ? nx : x;
+                    }
+#pragma unroll
+                    for (int c = 1; c < MAXCH; ++c) {
+                        const u64 y = x & (x - 1);
+                        x = (uint32_t)c <= r ? y : x;
+                    }
+                    v = 64 * wsel + (uint32_t)__ffsll((long long)x) - 1;
+                } else {
+                    v = e >> 16;
+                }
                 u64 C[RW];
 #pragma unroll
                 for (int w = 0; w < NW; ++w)
-                    C[w] = s_par[slot * RW + w];
-                C[NW] = s_par[slot * RW + NW] + s_key[v];
+                    C[w] = s_par[slot * PW + w];
+                C[NW] = s_par[slot * PW + NW] + s_key[v];
                 if (PACK) {
                     // child ids: (v1, v2) of the parent, last vertex v
                     const uint32_t v12 = packed_ids(C[NW - 1], idb) & ((1u << (2 * idb)) - 1);
@@ -1247,7 +1302,7 @@ size_t expand_smem(Mode m, int nw, int n, bool packed)
 {
     if (m == Mode::B) {
         const size_t tile = (size_t)kBlock * expand_paths_per_thread(nw);
-        return blocked_ring_bytes(nw, packed) + (size_t)n * (2 * nw + 1) * sizeof(u64) + tile * (nw + 1) * 8 +
+        return blocked_ring_bytes(nw, packed) + (size_t)n * (2 * nw + 1) * sizeof(u64) + tile * (2 * nw + 1) * 8 +
                (packed ? 0 : tile * 4) + (size_t)kChildCapX4 * tile;
     }
     const size_t kb = nw <= kByteTableWords ? (size_t)8 * nw * 256 : 0;
