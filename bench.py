@@ -272,15 +272,20 @@ def main():
     launches = sum(s["launches"] for s in stats)
     peak, peak_kind = peaks()
     achieved = (bytes_alg / (t_expand / 1e3)) / 1e9 if t_expand > 0 else 0.0
-    traffic = None
+    # traffic: dram__bytes_read.sum + dram__bytes_write.sum of one ncu --set full capture of this
+    # kernel (per launch), with the algorithmic bytes of that same launch (from the CC_TRACE log)
+    traffic = traffic_ratio = None
     tp = os.path.join(ROOT, "profiles", "ncu_traffic.json")
     if os.path.exists(tp):
         try:
-            traffic = json.load(open(tp)).get(args.workload)
+            t_ = json.load(open(tp)).get(args.workload)
+            if t_:
+                traffic, traffic_ratio = t_["dram_bytes"], t_["dram_over_alg"]
         except Exception:
-            traffic = None
+            traffic = traffic_ratio = None
     roofline = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
-                "frac": achieved / peak, "traffic": traffic, "peak_kind": peak_kind,
+                "frac": achieved / peak, "traffic": traffic, "traffic_over_alg": traffic_ratio,
+                "peak_kind": peak_kind,
                 "kernel": "k_expand_blocked" if g[0] <= 512 else "k_expand_wide", "expand_share_of_step": t_expand / dev_ms if dev_ms else None,
                 "bytes_alg_per_step": bytes_alg / args.steps}
 
