@@ -159,6 +159,22 @@ __device__ __forceinline__ u64 block_reserve2(unsigned int c, u64 *counter, Rese
     return sm.base + sm.warp[wid] + (incl - c);
 }
 
+// Row v of an n x NW shared-memory bit matrix; NW == 2 rows are read as one 128-bit LDS
+// (the tables start 16-byte aligned).
+template <int NW>
+__device__ __forceinline__ void lds_row(const u64 *base, uint32_t v, u64 (&r)[NW])
+{
+    if constexpr (NW == 2) {
+        const ulonglong2 t = reinterpret_cast<const ulonglong2 *>(base)[v];
+        r[0] = t.x;
+        r[1] = t.y;
+    } else {
+#pragma unroll
+        for (int w = 0; w < NW; ++w)
+            r[w] = base[v * NW + w];
+    }
+}
+
 // Split reservation.  reserve_begin: block scan (2 barriers) -> this thread's TILE-LOCAL offset;
 // the last lane of warp 0 issues the global atomicAdd and keeps its (in-flight) result in
 // *ticket.  That lane calls reserve_publish(ticket) later, after independent work, so the
@@ -518,7 +534,8 @@ __global__ void __launch_bounds__(kBlock, NW <= 2 ? 3 : 2) k_expand_blocked(cons
     char *ring = (char *)smem;
     u64 *s_adj = (u64 *)(ring + (size_t)kStages * kStageBytes);
     u64 *s_key = s_adj + p.g.n * NW;
-    u64 *s_above = s_key + p.g.n;  // s_above[v*NW + w] = word w of {x : x > v} (the label gate)
+    // s_above[v*NW + w] = word w of {x : x > v} (the label gate); 16-byte aligned (padded keys)
+    u64 *s_above = s_key + ((p.g.n + 1) & ~1);
     // staged children of one tile: parent state per path slot, one (slot, v) entry per child
     constexpr int PW = RW + NW;                           // parent child state + extension words
     u64 *s_par = s_above + p.g.n * NW;                    // [kTile][PW]
@@ -591,15 +608,18 @@ __global__ void __launch_bounds__(kBlock, NW <= 2 ? 3 : 2) k_expand_blocked(cons
             const uint32_t v1 = id[i] & idm;
             const uint32_t v2 = (id[i] >> idb) & idm;
             const uint32_t vt = id[i] >> (2 * idb);
-            u64 close[NW];
+            u64 close[NW], arow[NW], abv[NW], a1row[NW];
             bool any_close = false;
+            lds_row<NW>(s_adj, vt, arow);
+            lds_row<NW>(s_above, v2, abv);
+            lds_row<NW>(s_adj, v1, a1row);
 #pragma unroll
             for (int w = 0; w < NW; ++w) {
-                const u64 a = s_adj[vt * NW + w];
+                const u64 a = arow[w];
                 cand += __popcll(a);  // deg(vt): the candidate slots of Alg. 3 (statistic)
                 // the packed ids sit above bit n, where a is zero: they never leak into c
-                const u64 c = a & s_above[v2 * NW + w] & ~W[i][w];
-                const u64 a1 = s_adj[v1 * NW + w];
+                const u64 c = a & abv[w] & ~W[i][w];
+                const u64 a1 = a1row[w];
                 close[w] = c & a1;
                 ext[i][w] = p.emit ? (c & ~a1) : 0ull;
                 any_close |= close[w] != 0ull;
@@ -643,9 +663,11 @@ __global__ void __launch_bounds__(kBlock, NW <= 2 ? 3 : 2) k_expand_blocked(cons
                     continue;
                 const uint32_t slot = threadIdx.x + kBlock * i;
                 const uint32_t vt = id[i] >> (2 * idb);
+                u64 ar[NW];
+                lds_row<NW>(s_adj, vt, ar);
 #pragma unroll
                 for (int w = 0; w < NW; ++w)
-                    s_par[slot * PW + w] = W[i][w] | s_adj[vt * NW + w] | bit_in_word(w, vt);
+                    s_par[slot * PW + w] = W[i][w] | ar[w] | bit_in_word(w, vt);
                 s_par[slot * PW + NW] = W[i][NW];
                 if (!PACK)
                     s_pid[slot] = id[i] & ((1u << (2 * idb)) - 1);
@@ -723,16 +745,20 @@ __global__ void __launch_bounds__(kBlock, NW <= 2 ? 3 : 2) k_expand_blocked(cons
                 const uint32_t e = s_child[j];
                 const uint32_t slot = e & 0xffffu;
                 uint32_t v;
+                u64 par[PW];
+#pragma unroll
+                for (int w = 0; w < PW; ++w)
+                    par[w] = (w < RW || MAXCH > 0) ? s_par[slot * PW + w] : 0ull;
                 if (MAXCH > 0) {
                     // v = the rank-th (rank < MAXCH) set bit of the parent's extension words:
                     // pick the word by popcount, drop `rank` low bits (selects), find-first-set
                     uint32_t r = e >> 16;
-                    u64 x = s_par[slot * PW + RW];
+                    u64 x = par[RW];
                     uint32_t wsel = 0;
 #pragma unroll
                     for (int w = 1; w < NW; ++w) {
                         const uint32_t pc = __popcll(x);
-                        const u64 nx = s_par[slot * PW + RW + w];
+                        const u64 nx = par[RW + w];
                         const bool next = r >= pc;
                         r = next ? r - pc : r;
                         wsel = next ? (uint32_t)w : wsel;
@@ -750,8 +776,8 @@ __global__ void __launch_bounds__(kBlock, NW <= 2 ? 3 : 2) k_expand_blocked(cons
                 u64 C[RW];
 #pragma unroll
                 for (int w = 0; w < NW; ++w)
-                    C[w] = s_par[slot * PW + w];
-                C[NW] = s_par[slot * PW + NW] + s_key[v];
+                    C[w] = par[w];
+                C[NW] = par[NW] + s_key[v];
                 if (PACK) {
                     // child ids: (v1, v2) of the parent, last vertex v
                     const uint32_t v12 = packed_ids(C[NW - 1], idb) & ((1u << (2 * idb)) - 1);
@@ -1302,7 +1328,8 @@ size_t expand_smem(Mode m, int nw, int n, bool packed)
 {
     if (m == Mode::B) {
         const size_t tile = (size_t)kBlock * expand_paths_per_thread(nw);
-        return blocked_ring_bytes(nw, packed) + (size_t)n * (2 * nw + 1) * sizeof(u64) + tile * (2 * nw + 1) * 8 +
+        return blocked_ring_bytes(nw, packed) + ((size_t)n * 2 * nw + ((n + 1) & ~1)) * sizeof(u64) +
+               tile * (2 * nw + 1) * 8 +
                (packed ? 0 : tile * 4) + (size_t)kChildCapX4 * tile;
     }
     const size_t kb = nw <= kByteTableWords ? (size_t)8 * nw * 256 : 0;
