@@ -1,0 +1,38 @@
+"""Small enumerations through every kernel class, for compute-sanitizer runs:
+    compute-sanitizer --tool memcheck python tools/sanitize_run.py
+Exits non-zero if any result differs from the oracle."""
+import os
+import sys
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+
+import torch  # noqa: E402
+
+import oracle  # noqa: E402
+from paper_1410_4876_b200 import binding, inputs as I  # noqa: E402
+
+ws = torch.empty(64 << 20, dtype=torch.uint8, device="cuda")
+cases = [
+    ("p6x6 count (B-mode, Delta<=4 kernel)", I.grid(6, 6), {}),
+    ("p5x5 collect (S-mode thread kernel)", I.grid(5, 5), dict(collect=True)),
+    ("k12x12 count (B-mode, Delta>4)", I.complete_bipartite(12, 12), {}),
+    ("k40x40 collect (S-mode warp kernel)", I.complete_bipartite(40, 40), dict(collect=True)),
+    ("gnp200 count shard 1/3 (filter kernel)", I.gnp(200, 0.04, 3), dict(max_len=8, shard_index=1, shard_count=3,
+                                                                          min_shard_paths=16)),
+    ("gnp600 count (wide class)", I.gnp(600, 0.01, 5), dict(max_len=8)),
+    ("gnp600 count shard 0/2 (wide filter)", I.gnp(600, 0.01, 5), dict(max_len=7, shard_index=0, shard_count=2,
+                                                                        min_shard_paths=16)),
+]
+bad = 0
+for name, g, kw in cases:
+    got = binding.enumerate_cycles(*g, workspace=ws, **kw)
+    okw = {k: v for k, v in kw.items() if k in ("max_len", "collect")}
+    if "shard_count" in kw:
+        print(name, "ran; cycles on this shard:", int(got["counts"].sum()))
+        continue
+    want = oracle.enumerate_cycles(*g, **okw)
+    same = got["counts"].tolist() == want["counts"].tolist() and got["set_hash"] == want["set_hash"]
+    print(name, "OK" if same else "MISMATCH", int(got["counts"].sum()))
+    bad += not same
+sys.exit(1 if bad else 0)
