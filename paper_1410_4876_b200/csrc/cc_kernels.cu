@@ -1128,9 +1128,12 @@ __global__ void __launch_bounds__(kBlock) k_stage1_wide(const LaunchArgs p)
 
 constexpr int kWidePaths = 4;  // paths per warp per tile in k_expand_wide
 
+constexpr int kWideVList = 256;  // child-vertex list per warp (children of one path)
+
 __global__ void __launch_bounds__(kBlock) k_expand_wide(const LaunchArgs p)
 {
     __shared__ ReserveSmem rs;
+    __shared__ uint32_t s_vlist[(kBlock / 32) * kWideVList];
     const int NW = p.g.nw, RW = NW + 1;
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
     const uint32_t idb = p.idb, idm = (1u << idb) - 1;
@@ -1141,8 +1144,20 @@ __global__ void __launch_bounds__(kBlock) k_expand_wide(const LaunchArgs p)
     u64 cnt = 0, hs = 0, cand = 0;
     for (u64 tb = (u64)blockIdx.x * kTilePaths; tb < p.n_in; tb += (u64)gridDim.x * kTilePaths) {
         u64 ext[kWidePaths], Cw[kWidePaths], ksv[kWidePaths];
-        u64 v12v[kWidePaths];
+        u64 v12v[kWidePaths], Bv[kWidePaths], KSv[kWidePaths];
         unsigned int ne = 0;
+        // issue the loads of all the warp's records first (independent, in flight together)
+#pragma unroll
+        for (int i = 0; i < kWidePaths; ++i) {
+            const u64 r = tb + (u64)wid * kWidePaths + i;
+            Bv[i] = 0;
+            KSv[i] = 0;
+            if (r < p.n_in) {
+                const u64 *rec = wide_rec(p.pg, p.pg.in_pages, r, RW);
+                Bv[i] = mine ? rec[lane] : 0ull;
+                KSv[i] = lane == 0 ? rec[NW] : 0ull;
+            }
+        }
 #pragma unroll
         for (int i = 0; i < kWidePaths; ++i) {
             ext[i] = 0;
@@ -1152,9 +1167,8 @@ __global__ void __launch_bounds__(kBlock) k_expand_wide(const LaunchArgs p)
             const u64 r = tb + (u64)wid * kWidePaths + i;
             if (r >= p.n_in)
                 continue;  // warp-uniform
-            const u64 *rec = wide_rec(p.pg, p.pg.in_pages, r, RW);
-            const u64 B = mine ? rec[lane] : 0ull;
-            const u64 ks = __shfl_sync(FULL_MASK, lane == 0 ? rec[NW] : 0ull, 0);
+            const u64 B = Bv[i];
+            const u64 ks = __shfl_sync(FULL_MASK, KSv[i], 0);
             const u64 id = packed_ids(__shfl_sync(FULL_MASK, B, NW - 1), idb);
             const uint32_t v1 = (uint32_t)(id & idm), v2 = (uint32_t)((id >> idb) & idm),
                            vt = (uint32_t)(id >> (2 * idb));
@@ -1188,25 +1202,79 @@ __global__ void __launch_bounds__(kBlock) k_expand_wide(const LaunchArgs p)
             continue;
         }
         u64 o = p.out_off + off;
+        uint32_t *sv = s_vlist + wid * kWideVList;
 #pragma unroll
         for (int i = 0; i < kWidePaths; ++i) {
-            u64 m = ext[i];
-            for (;;) {
-                const unsigned int has = __ballot_sync(FULL_MASK, m != 0ull);
-                if (!has)
-                    break;
-                const int L = __ffs(has) - 1;  // lowest word with a child
-                const int b = __shfl_sync(FULL_MASK, __ffsll((long long)m) - 1, L);
-                if (lane == L)
-                    m &= m - 1;
-                const uint32_t v = (uint32_t)(64 * L + b);
-                u64 *rec = wide_rec(p.pg, p.pg.out_pages, o, RW);
-                if (mine)
-                    rec[lane] = lane == NW - 1 ? with_packed_ids(Cw[i], v12v[i] | ((u64)v << (2 * idb)), idb) : Cw[i];
-                if (lane == 0)
-                    rec[NW] = ksv[i] + __ldg(key + v);
-                ++o;
+            // children of path i: every child record equals (B | N[vt]) except the packed-id word
+            // (last vertex v) and the keysum word (ks + key(v)).  Lanes publish the child
+            // vertices in order into this warp's list; then lane w writes the common word w of
+            // all children (stride RW words) and lanes e write the keysum word of child e.
+            const uint32_t pc = __popcll(ext[i]);
+            unsigned int incl = pc;
+#pragma unroll
+            for (int d = 1; d < 32; d <<= 1) {
+                const unsigned int t = __shfl_up_sync(FULL_MASK, incl, d);
+                if (lane >= d)
+                    incl += t;
             }
+            const unsigned int E = __shfl_sync(FULL_MASK, incl, 31);
+            if (E == 0)
+                continue;
+            if (E > kWideVList) {
+                // very high fan-out (> kWideVList children of one path): one child at a time
+                u64 m = ext[i];
+                for (;;) {
+                    const unsigned int has = __ballot_sync(FULL_MASK, m != 0ull);
+                    if (!has)
+                        break;
+                    const int L = __ffs(has) - 1;
+                    const int b = __shfl_sync(FULL_MASK, __ffsll((long long)m) - 1, L);
+                    if (lane == L)
+                        m &= m - 1;
+                    const uint32_t v = (uint32_t)(64 * L + b);
+                    u64 *rec = wide_rec(p.pg, p.pg.out_pages, o, RW);
+                    if (mine)
+                        rec[lane] = lane == NW - 1 ? with_packed_ids(Cw[i], v12v[i] | ((u64)v << (2 * idb)), idb) : Cw[i];
+                    if (lane == 0)
+                        rec[NW] = ksv[i] + __ldg(key + v);
+                    ++o;
+                }
+                continue;
+            }
+            {
+                u64 m = ext[i];
+                unsigned int pos = incl - pc;
+                while (m) {
+                    const int b = __ffsll((long long)m) - 1;
+                    m &= m - 1;
+                    sv[pos++] = (uint32_t)(64 * lane + b);
+                }
+            }
+            __syncwarp();
+            const uint32_t pg_mask = (1u << p.pg.log_p) - 1;
+            const uint32_t slot0 = (uint32_t)(o & pg_mask);
+            if (slot0 + E <= pg_mask + 1) {
+                // all E children in one page: plain strided stores, one loop for every lane
+                u64 *rec0 = wide_rec(p.pg, p.pg.out_pages, o, RW);
+                if (mine) {
+                    const bool idw = lane == NW - 1;
+                    u64 *q = rec0 + lane;
+                    for (unsigned int e = 0; e < E; ++e, q += RW)
+                        *q = idw ? with_packed_ids(Cw[i], v12v[i] | ((u64)sv[e] << (2 * idb)), idb) : Cw[i];
+                }
+                for (unsigned int e = lane; e < E; e += 32)
+                    rec0[(u64)e * RW + NW] = ksv[i] + __ldg(key + sv[e]);
+            } else {
+                for (unsigned int e = 0; e < E; ++e) {
+                    u64 *rec = wide_rec(p.pg, p.pg.out_pages, o + e, RW);
+                    if (mine)
+                        rec[lane] = lane == NW - 1 ? with_packed_ids(Cw[i], v12v[i] | ((u64)sv[e] << (2 * idb)), idb) : Cw[i];
+                    if (lane == 0)
+                        rec[NW] = ksv[i] + __ldg(key + sv[e]);
+                }
+            }
+            o += E;
+            __syncwarp();
         }
     }
     if (!p.count)
