@@ -109,6 +109,10 @@ typedef struct {
     double t_stage1_ms;           /* profile=1: summed CUDA-event time of Stage 1 launches */
     double t_labeling_ms;         /* host degree labelling + graph build (cc_graph_from_csr) */
     double t_wall_ms;             /* host wall time of cc_enumerate */
+    uint64_t leaf_paths;          /* count mode with max_len: paths of the last level (their
+                                     children could not close within max_len) counted by the
+                                     launch that created them and never written */
+    uint64_t paths_written;       /* frontier records written by Stage 1 and Stage 2 */
 } cc_stats;
 
 /* Fills *opt with defaults (device -1, stream NULL, no cap, count-only, one shard). */

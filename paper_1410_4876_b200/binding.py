@@ -62,6 +62,7 @@ class cc_stats(ctypes.Structure):
         ("d2h_bytes", ctypes.c_uint64), ("t_dev_ms", ctypes.c_double),
         ("t_expand_ms", ctypes.c_double), ("t_stage1_ms", ctypes.c_double),
         ("t_labeling_ms", ctypes.c_double), ("t_wall_ms", ctypes.c_double),
+        ("leaf_paths", ctypes.c_uint64), ("paths_written", ctypes.c_uint64),
     ]
 
 

@@ -482,7 +482,7 @@ static cc_status enumerate_impl(const cc_graph *cg, const cc_options *opt_in, cc
     cc_result *res = new cc_result();
     std::unique_ptr<cc_result, void (*)(cc_result *)> res_guard(res, cc_result_free);
     res->n = n;
-    res->counts.assign(n + 2, 0);
+    res->counts.assign(n + 3, 0);
     res->paths.assign(n + 2, 0);
     res->cand.assign(n + 2, 0);
     res->device = device;
@@ -647,9 +647,13 @@ static cc_status enumerate_impl(const cc_graph *cg, const cc_options *opt_in, cc
     }
     enum Kind { STAGE1, EXPAND, FILTER };
     int trace_level = 0;
+    // emit: the launch creates paths (children / triplets); leaf: last-level fusion (count the
+    // children, write none -- cc::Scratch)
     auto launch = [&](Kind kind, const uint32_t *in, size_t n_in_pages, u64 n_in, u64 pair_lo, bool emit,
-                      bool count, bool filter, std::vector<uint32_t> &used, bool *overflow) -> cc_status {
+                      bool leaf, bool count, bool filter, std::vector<uint32_t> &used,
+                      bool *overflow) -> cc_status {
         *overflow = false;
+        const bool writes = emit && !leaf;
         const size_t nfree = free_pages.size();
         // page table: input pages, then every free page (in pop order) as potential output
         for (size_t i = 0; i < n_in_pages; ++i)
@@ -658,16 +662,17 @@ static cc_status enumerate_impl(const cc_graph *cg, const cc_options *opt_in, cc
             h_tab[npages + i] = free_pages[nfree - 1 - i];
         if (n_in_pages)
             CC_CUDA(cudaMemcpyAsync(d_tab, h_tab, n_in_pages * 4, cudaMemcpyHostToDevice, st));
-        if (emit && nfree)
+        if (writes && nfree)
             CC_CUDA(cudaMemcpyAsync(d_tab + npages, h_tab + npages, nfree * 4, cudaMemcpyHostToDevice, st));
-        S.h2d_bytes += (n_in_pages + (emit ? nfree : 0)) * 4;
+        S.h2d_bytes += (n_in_pages + (writes ? nfree : 0)) * 4;
         CC_CUDA(cudaMemsetAsync(d_sc, 0, offsetof(cc::Scratch, cyc_count), st));
         cc::LaunchArgs a = base;
         a.in_lo = pair_lo;
         a.n_in = n_in;
         a.out_off = 0;
-        a.out_cap = emit ? nfree * P : 0;
+        a.out_cap = writes ? nfree * P : 0;
         a.emit = emit ? 1 : 0;
+        a.emit_next = leaf ? 0 : 1;
         a.count = count ? 1 : 0;
         a.filter = filter ? 1 : 0;
         if (opt.profile)
@@ -699,7 +704,8 @@ static cc_status enumerate_impl(const cc_graph *cg, const cc_options *opt_in, cc
             std::fprintf(trace.f, "%s,%d,%llu,%llu,%llu,%llu,%.6f,%d\n",
                          kind == STAGE1 ? "stage1" : kind == EXPAND ? "expand" : "filter", trace_level,
                          (unsigned long long)n_in, (unsigned long long)h_sc->out_count,
-                         (unsigned long long)h_sc->cycles, (unsigned long long)h_sc->cand, ms,
+                         (unsigned long long)(h_sc->cycles + h_sc->cycles_next),
+                         (unsigned long long)(h_sc->cand + h_sc->cand_next), ms,
                          (h_sc->err || h_sc->out_count > a.out_cap) ? 1 : 0);
         if (h_sc->err || h_sc->out_count > a.out_cap) {
             *overflow = true;
@@ -710,6 +716,8 @@ static cc_status enumerate_impl(const cc_graph *cg, const cc_options *opt_in, cc
             return CC_OK;
         }
         cyc_committed = h_sc->cyc_count;
+        if (kind != FILTER)
+            S.paths_written += h_sc->out_count;
         const u64 npg = (h_sc->out_count + P - 1) / P;
         used.clear();
         for (u64 i = 0; i < npg; ++i) {
@@ -743,7 +751,7 @@ static cc_status enumerate_impl(const cc_graph *cg, const cc_options *opt_in, cc
                 return fail(CC_ERR_CAPACITY, "no free arena page for Stage 1");
             bool of = false;
             trace_level = 2;
-            cc_status s = launch(STAGE1, nullptr, 0, c, s1_next, want_paths, count_tri, s1_filter, used, &of);
+            cc_status s = launch(STAGE1, nullptr, 0, c, s1_next, want_paths, false, count_tri, s1_filter, used, &of);
             if (s != CC_OK)
                 return s;
             if (of)
@@ -766,7 +774,8 @@ static cc_status enumerate_impl(const cc_graph *cg, const cc_options *opt_in, cc
         if (W > 1 && !L.sharded && L.count >= shard_threshold) {
             bool of = false;
             trace_level = d;
-            cc_status s = launch(FILTER, L.pages.data(), L.pages.size(), L.count, 0, true, false, false, used, &of);
+            cc_status s = launch(FILTER, L.pages.data(), L.pages.size(), L.count, 0, true, false, false, false, used,
+                                 &of);
             if (s != CC_OK)
                 return s;
             if (of)
@@ -781,15 +790,20 @@ static cc_status enumerate_impl(const cc_graph *cg, const cc_options *opt_in, cc
             continue;
         }
         const bool owner = W == 1 || L.sharded || opt.shard_index == 0;
+        // children of F_d have d+1 vertices: created iff d+1 < max_len.  Count mode fuses the
+        // last level: if they could not have children themselves (d+2 >= max_len) they are
+        // counted by this launch and not written
         const bool emit = max_len == 0 || (u64)d + 1 < max_len;
+        const bool leaf = emit && mode == cc::Mode::B && max_len != 0 && (u64)d + 2 >= max_len;
+        const bool writes = emit && !leaf;
         Level &C = levels[d + 1];
-        if (emit && !C.init) {
+        if (writes && !C.init) {
             C.init = true;
             C.sharded = L.sharded;
         }
         // ---- choose the input chunk: the last k pages of F_d
         size_t k = L.pages.size();
-        if (emit && (W == 1 || L.sharded)) {
+        if (writes && (W == 1 || L.sharded)) {
             double f = L.fan > 0 ? L.fan * 1.15 : (levels[d - 1].fan > 0 ? levels[d - 1].fan * 1.5 : maxfan);
             f = std::min(std::max(f, 0.05), maxfan);
             // keep a reserve so that the child level can expand its first page next (about
@@ -813,7 +827,7 @@ static cc_status enumerate_impl(const cc_graph *cg, const cc_options *opt_in, cc
             const uint32_t *in = L.pages.data() + (L.pages.size() - k);
             bool of = false;
             trace_level = d;
-            cc_status s = launch(EXPAND, in, k, c, 0, emit, owner, false, used, &of);
+            cc_status s = launch(EXPAND, in, k, c, 0, emit, leaf, owner, false, used, &of);
             if (s != CC_OK)
                 return s;
             if (of) {
@@ -841,6 +855,13 @@ static cc_status enumerate_impl(const cc_graph *cg, const cc_options *opt_in, cc
                 S.paths_expanded += c;
                 res->counts[d + 1] += h_sc->cycles;
                 res->hash += h_sc->hash;
+                if (leaf) {  // the children: counted here, never written
+                    res->paths[d + 1] += h_sc->paths_next;
+                    res->cand[d + 1] += h_sc->cand_next;
+                    res->counts[d + 2] += h_sc->cycles_next;
+                    S.paths_expanded += h_sc->paths_next;
+                    S.leaf_paths += h_sc->paths_next;
+                }
             }
             S.bytes_alg += (c + h_sc->out_count) * rec_bytes;
             if (c > 0)

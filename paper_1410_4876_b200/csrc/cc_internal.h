@@ -69,12 +69,19 @@ struct CycleStore {
 
 // Per-launch scratch accumulators (zeroed before, read back after every launch, so a launch
 // that overflows its output can be discarded without touching the totals).
+// Last-level fusion (count mode, with a length cap K): when the children of F_t cannot have
+// children of their own (t + 2 >= K), the expansion of F_t does not write them; it counts them
+// (|F_{t+1}|, their candidate slots) and their closures (cycles of t+2 vertices) at once in the
+// *_next counters.  The deepest frontier level is then never materialised.
 struct Scratch {
     u64 out_count;               // records demanded by this launch (keeps counting past out_cap)
     u64 err;                     // bit 0: output overflow
-    u64 cycles;                  // closures counted by this launch (all of one length)
-    u64 hash;                    // sum of h(C) over those closures (mod 2^64)
-    u64 cand;                    // candidate slots scanned
+    u64 cycles;                  // closures of the input paths (all of one length t+1)
+    u64 hash;                    // sum of h(C) over every closure counted by the launch (mod 2^64)
+    u64 cand;                    // candidate slots of the input paths
+    u64 cycles_next;             // last-level fusion: closures of the children (t+2 vertices)
+    u64 cand_next;               // last-level fusion: candidate slots of the children
+    u64 paths_next;              // last-level fusion: children counted (|F_{t+1}| share)
     u64 cyc_count;               // collect-mode store counter (NOT reset per launch)
 };
 
@@ -87,7 +94,8 @@ struct LaunchArgs {
     uint64_t n_in;               // input records (or pairs)
     uint64_t out_off;            // first virtual output position in out_pages
     uint64_t out_cap;            // positions available from out_off
-    int32_t emit;                // 1 = write extended paths / triplets
+    int32_t emit;                // 1 = create extended paths / triplets
+    int32_t emit_next;           // 0 with emit = 1: last-level fusion (count the children, write none)
     int32_t count;               // 1 = this shard owns (counts) the closures of this launch
     int32_t collect;             // 1 = store closed cycles
     int32_t filter;              // 1 = keep only records of this shard (Stage 1 / filter kernel)

@@ -53,6 +53,13 @@ __device__ __forceinline__ u64 bit_in_word(int w, uint32_t v)
     return (w == (int)(v >> 6)) ? (1ull << (v & 63)) : 0ull;
 }
 
+// word w of the label gate {x : x > v2} (Alg. 3 line 11 after relabelling)
+__device__ __forceinline__ u64 above_word(uint32_t v2, int w)
+{
+    const int sh = (int)v2 + 1 - 64 * w;
+    return sh <= 0 ? ~0ull : (sh >= 64 ? 0ull : (~0ull << sh));
+}
+
 // ---------------------------------------------------------------------------- paged records
 __device__ __forceinline__ char *page_ptr(const Pages &pg, uint32_t page)
 {
@@ -299,37 +306,45 @@ __device__ __forceinline__ u64 keysum(const u64 (&S)[NW], const u64 *s_key, cons
     return ks;
 }
 
-// Block-reduce (cycles, hash, cand) into the launch scratch (one atomic each per CTA).
-__device__ __forceinline__ void flush_accum(u64 cnt, u64 hs, u64 cand, Scratch *sc)
+// Per-thread accumulators of a launch, block-reduced into the Scratch at the end (one atomic
+// per counter per CTA).  *_next are the lookahead counters (see Scratch).
+struct Acc {
+    u64 cyc = 0, hash = 0, cand = 0, cyc_next = 0, cand_next = 0, paths_next = 0;
+};
+
+__device__ __forceinline__ void flush(Acc a, Scratch *sc)
 {
-    __shared__ u64 red[3][kBlock / 32];
+    constexpr int K = 6;
+    __shared__ u64 red[K][kBlock / 32];
+    u64 v[K] = {a.cyc, a.hash, a.cand, a.cyc_next, a.cand_next, a.paths_next};
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
 #pragma unroll
-    for (int o = 16; o > 0; o >>= 1) {
-        cnt += __shfl_xor_sync(FULL_MASK, cnt, o);
-        hs += __shfl_xor_sync(FULL_MASK, hs, o);
-        cand += __shfl_xor_sync(FULL_MASK, cand, o);
-    }
-    if (lane == 0) {
-        red[0][wid] = cnt;
-        red[1][wid] = hs;
-        red[2][wid] = cand;
+    for (int k = 0; k < K; ++k) {
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1)
+            v[k] += __shfl_xor_sync(FULL_MASK, v[k], o);
+        if (lane == 0)
+            red[k][wid] = v[k];
     }
     __syncthreads();
-    if (threadIdx.x == 0) {
-        u64 a = 0, b = 0, c = 0;
-        for (int i = 0; i < kBlock / 32; ++i) {
-            a += red[0][i];
-            b += red[1][i];
-            c += red[2][i];
-        }
-        if (a)
-            atomicAdd(&sc->cycles, a);
-        if (b)
-            atomicAdd(&sc->hash, b);
-        if (c)
-            atomicAdd(&sc->cand, c);
+    if (threadIdx.x < K) {
+        u64 s = 0;
+        for (int i = 0; i < kBlock / 32; ++i)
+            s += red[threadIdx.x][i];
+        // the six counters are consecutive u64 fields of Scratch starting at `cycles`
+        static_assert(offsetof(Scratch, paths_next) - offsetof(Scratch, cycles) == 5 * sizeof(u64), "Scratch layout");
+        if (s)
+            atomicAdd(&sc->cycles + threadIdx.x, s);
     }
+}
+
+__device__ __forceinline__ void flush_accum(u64 cnt, u64 hs, u64 cand, Scratch *sc)
+{
+    Acc a;
+    a.cyc = cnt;
+    a.hash = hs;
+    a.cand = cand;
+    flush(a, sc);
 }
 
 // Graph tables staged in shared memory: adjacency bit rows (n*NW words), keys (n words) and,
@@ -521,7 +536,7 @@ __host__ __device__ constexpr size_t blocked_stage_bytes()
 
 // MAXCH > 0: every path has at most MAXCH children (Delta - 1, host-checked), so the staging of
 // children is unrolled into MAXCH predicated steps instead of a divergent per-bit loop.
-template <int NW, int MAXCH, bool PACK>
+template <int NW, int MAXCH, bool PACK, bool LEAF>
 __global__ void __launch_bounds__(kBlock, NW <= 2 ? 3 : 2) k_expand_blocked(const LaunchArgs p)
 {
     constexpr int RW = NW + 1;
@@ -579,6 +594,10 @@ __global__ void __launch_bounds__(kBlock, NW <= 2 ? 3 : 2) k_expand_blocked(cons
     stage_graph<NW, false>(p.g, s_adj, s_key, nullptr);  // includes __syncthreads
 
     u64 cnt = 0, hs = 0, cand = 0;
+    u64 leaf_paths = 0, leaf_cand = 0, leaf_cyc = 0;
+    // last level (p.emit && !p.emit_next): the children <p,v> cannot have children within the
+    // length cap; they are counted -- |F_{t+1}|, deg(v), their closures -- and not written
+    constexpr bool leaf = LEAF;  // launched iff p.emit && !p.emit_next
     for (u64 k = 0; k < my_tiles; ++k) {
         const int st = (int)(k % kStages);
         const u64 base = (blockIdx.x + k * gridDim.x) * (u64)kTile;
@@ -637,6 +656,44 @@ __global__ void __launch_bounds__(kBlock, NW <= 2 ? 3 : 2) k_expand_blocked(cons
                         hs += mix64(ks + s_key[64 * w + b]);
                     }
                 }
+            }
+            if constexpr (LEAF) {
+                // Close(<p,v>) = Adj(v) & Z(p), Z(p) = {x > v2} & ~(B | N[vt]) & Adj(v1)
+                u64 Z[NW];
+#pragma unroll
+                for (int w = 0; w < NW; ++w) {
+                    Z[w] = abv[w] & ~(W[i][w] | arow[w] | bit_in_word(w, vt)) & a1row[w];
+                    ne -= __popcll(ext[i][w]);
+                }
+                if (p.count) {
+#pragma unroll
+                    for (int w = 0; w < NW; ++w) {
+                        u64 m = ext[i][w];
+                        while (m) {
+                            const int b = __ffsll((long long)m) - 1;
+                            m &= m - 1;
+                            const uint32_t v = (uint32_t)(64 * w + b);
+                            u64 av[NW];
+                            lds_row<NW>(s_adj, v, av);
+                            const u64 ksv = W[i][NW] + s_key[v];
+                            leaf_paths++;
+#pragma unroll
+                            for (int w2 = 0; w2 < NW; ++w2) {
+                                leaf_cand += __popcll(av[w2]);
+                                u64 cl = av[w2] & Z[w2];
+                                leaf_cyc += __popcll(cl);
+                                while (cl) {
+                                    const int b2 = __ffsll((long long)cl) - 1;
+                                    cl &= cl - 1;
+                                    hs += mix64(ksv + s_key[64 * w2 + b2]);
+                                }
+                            }
+                        }
+                    }
+                }
+#pragma unroll
+                for (int w = 0; w < NW; ++w)
+                    ext[i][w] = 0;
             }
         }
         // every thread has read stage st (the reservation starts with a barrier) -> refill it
@@ -791,7 +848,14 @@ __global__ void __launch_bounds__(kBlock, NW <= 2 ? 3 : 2) k_expand_blocked(cons
     }
     if (!p.count)
         cand = 0;
-    flush_accum(cnt, hs, cand, p.sc);
+    Acc a;
+    a.cyc = cnt;
+    a.hash = hs;
+    a.cand = cand;
+    a.cyc_next = leaf_cyc;
+    a.cand_next = leaf_cand;
+    a.paths_next = leaf_paths;
+    flush(a, p.sc);
 }
 
 // ---------------------------------------------------------------------------- Stage 2, S-mode
@@ -1042,12 +1106,6 @@ __device__ __forceinline__ u64 *wide_rec(const Pages &pg, const uint32_t *pages,
            (r & ((1ull << pg.log_p) - 1)) * (u64)RW;
 }
 
-__device__ __forceinline__ u64 above_word(uint32_t v2, int w)
-{
-    const int sh = (int)v2 + 1 - 64 * w;
-    return sh <= 0 ? ~0ull : (sh >= 64 ? 0ull : (~0ull << sh));
-}
-
 __global__ void __launch_bounds__(kBlock) k_stage1_wide(const LaunchArgs p)
 {
     __shared__ ReserveSmem rs;
@@ -1129,11 +1187,14 @@ __global__ void __launch_bounds__(kBlock) k_stage1_wide(const LaunchArgs p)
 constexpr int kWidePaths = 4;  // paths per warp per tile in k_expand_wide
 
 constexpr int kWideVList = 256;  // child-vertex list per warp (children of one path)
+constexpr int kWideZList = 32;   // closer list Z(p) per warp (last-level fusion)
 
+template <bool LEAF>
 __global__ void __launch_bounds__(kBlock) k_expand_wide(const LaunchArgs p)
 {
     __shared__ ReserveSmem rs;
     __shared__ uint32_t s_vlist[(kBlock / 32) * kWideVList];
+    __shared__ uint32_t s_zlist[(kBlock / 32) * kWideZList];
     const int NW = p.g.nw, RW = NW + 1;
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
     const uint32_t idb = p.idb, idm = (1u << idb) - 1;
@@ -1141,7 +1202,14 @@ __global__ void __launch_bounds__(kBlock) k_expand_wide(const LaunchArgs p)
     const u64 *__restrict__ key = p.g.key;
     const bool mine = lane < NW;  // this lane owns word `lane` of every record
     constexpr u64 kTilePaths = (u64)(kBlock / 32) * kWidePaths;
+    // last level (p.emit && !p.emit_next): the children are counted, not written (see
+    // k_expand_blocked); their closures Adj(v) & Z(p) are found by probing the few closers z in
+    // Z(p) (a list in shared memory) against row v, one bit test each
+    constexpr bool leaf = LEAF;  // launched iff p.emit && !p.emit_next
+    uint32_t *sv = s_vlist + wid * kWideVList;
+    uint32_t *sz = s_zlist + wid * kWideZList;
     u64 cnt = 0, hs = 0, cand = 0;
+    u64 leaf_paths = 0, leaf_cand = 0, leaf_cyc = 0;
     for (u64 tb = (u64)blockIdx.x * kTilePaths; tb < p.n_in; tb += (u64)gridDim.x * kTilePaths) {
         u64 ext[kWidePaths], Cw[kWidePaths], ksv[kWidePaths];
         u64 v12v[kWidePaths], Bv[kWidePaths], KSv[kWidePaths];
@@ -1186,11 +1254,94 @@ __global__ void __launch_bounds__(kBlock) k_expand_wide(const LaunchArgs p)
                     hs += mix64(ks + __ldg(key + 64 * lane + b));
                 }
             }
-            ne += __reduce_add_sync(FULL_MASK, (unsigned int)__popcll(ext[i]));
+            const unsigned int E = __reduce_add_sync(FULL_MASK, (unsigned int)__popcll(ext[i]));
             // the children's blocked set: vt becomes interior -> B | N[vt]
             Cw[i] = mine ? (B | a | bit_in_word(lane, vt)) : 0ull;
             ksv[i] = ks;
             v12v[i] = id & ((1ull << (2 * idb)) - 1);
+            if constexpr (!LEAF) {
+                ne += E;
+            } else if (E && p.count) {
+                const u64 Zw = mine ? (above_word(v2, lane) & ~Cw[i] & a1) : 0ull;
+                const unsigned int pz = __popcll(Zw);
+                unsigned int zincl = pz;
+#pragma unroll
+                for (int d = 1; d < 32; d <<= 1) {
+                    const unsigned int t = __shfl_up_sync(FULL_MASK, zincl, d);
+                    if (lane >= d)
+                        zincl += t;
+                }
+                const unsigned int nz = __shfl_sync(FULL_MASK, zincl, 31);
+                if (nz <= (unsigned int)kWideZList) {
+                    u64 m = Zw;
+                    unsigned int pos = zincl - pz;
+                    while (m) {
+                        const int b = __ffsll((long long)m) - 1;
+                        m &= m - 1;
+                        sz[pos++] = (uint32_t)(64 * lane + b);
+                    }
+                }
+                // the children in batches that fit the vertex list: all lanes, or 8 groups of
+                // 4 lanes (a lane holds at most 64 children)
+                const int ngroups = E <= (unsigned int)kWideVList ? 1 : 8;
+                for (int gi = 0; gi < ngroups; ++gi) {
+                    const bool inb = ngroups == 1 || (lane >> 2) == gi;
+                    const uint32_t pc = inb ? __popcll(ext[i]) : 0u;
+                    unsigned int incl = pc;
+#pragma unroll
+                    for (int d = 1; d < 32; d <<= 1) {
+                        const unsigned int t = __shfl_up_sync(FULL_MASK, incl, d);
+                        if (lane >= d)
+                            incl += t;
+                    }
+                    const unsigned int Eb = __shfl_sync(FULL_MASK, incl, 31);
+                    if (Eb == 0)
+                        continue;
+                    if (inb) {
+                        u64 m = ext[i];
+                        unsigned int pos = incl - pc;
+                        while (m) {
+                            const int b = __ffsll((long long)m) - 1;
+                            m &= m - 1;
+                            sv[pos++] = (uint32_t)(64 * lane + b);
+                        }
+                    }
+                    __syncwarp();
+                    if (lane == 0)
+                        leaf_paths += Eb;
+                    for (unsigned int e = lane; e < Eb; e += 32) {
+                        const uint32_t v = sv[e];
+                        leaf_cand += __ldg(p.g.rowptr + v + 1) - __ldg(p.g.rowptr + v);
+                    }
+                    if (nz <= (unsigned int)kWideZList) {
+                        for (unsigned int e = lane; e < Eb; e += 32) {
+                            const uint32_t v = sv[e];
+                            const u64 kv = ks + __ldg(key + v);
+                            const u64 *row = adj + (u64)v * NW;
+                            for (unsigned int q = 0; q < nz; ++q) {
+                                const uint32_t z = sz[q];
+                                if ((__ldg(row + (z >> 6)) >> (z & 63)) & 1ull) {
+                                    leaf_cyc++;
+                                    hs += mix64(kv + __ldg(key + z));
+                                }
+                            }
+                        }
+                    } else {
+                        for (unsigned int e = 0; e < Eb; ++e) {
+                            const uint32_t v = sv[e];
+                            u64 cl = mine ? (__ldg(adj + (u64)v * NW + lane) & Zw) : 0ull;
+                            leaf_cyc += __popcll(cl);
+                            const u64 kv = ks + __ldg(key + v);
+                            while (cl) {
+                                const int b = __ffsll((long long)cl) - 1;
+                                cl &= cl - 1;
+                                hs += mix64(kv + __ldg(key + 64 * lane + b));
+                            }
+                        }
+                    }
+                    __syncwarp();
+                }
+            }
         }
         // one reservation per CTA tile; the warp's count is carried by its lane 0
         const u64 off = __shfl_sync(FULL_MASK, block_reserve(lane == 0 ? ne : 0u, &p.sc->out_count, rs), 0);
@@ -1279,7 +1430,14 @@ __global__ void __launch_bounds__(kBlock) k_expand_wide(const LaunchArgs p)
     }
     if (!p.count)
         cand = 0;
-    flush_accum(cnt, hs, cand, p.sc);
+    Acc acc;
+    acc.cyc = cnt;
+    acc.hash = hs;
+    acc.cand = cand;
+    acc.cyc_next = leaf_cyc;
+    acc.cand_next = leaf_cand;
+    acc.paths_next = leaf_paths;
+    flush(acc, p.sc);
 }
 
 __global__ void __launch_bounds__(kBlock) k_shard_filter_wide(const LaunchArgs p)
@@ -1434,7 +1592,7 @@ static inline unsigned int grid_for(u64 items_per_block, u64 n, int grid_cap)
 
 // kernel for (which, mode, nw, packed); which: 0 stage1, 1 expand thread, 2 expand warp,
 // 3 filter, 4 expand with at most 3 children per path
-static KernelFn kernel_for(int which, Mode m, int nw, bool pk)
+static KernelFn kernel_for(int which, Mode m, int nw, bool pk, bool leaf = false)
 {
     const bool bm = m == Mode::B;
     switch (which) {
@@ -1447,7 +1605,8 @@ static KernelFn kernel_for(int which, Mode m, int nw, bool pk)
     case 2:
 #define K1(N)                                                                                            \
     if (nw == N)                                                                                         \
-        return bm ? (pk ? k_expand_blocked<N, 0, true> : k_expand_blocked<N, 0, false>)                  \
+        return bm ? (leaf ? (pk ? k_expand_blocked<N, 0, true, true> : k_expand_blocked<N, 0, false, true>)    \
+                          : (pk ? k_expand_blocked<N, 0, true, false> : k_expand_blocked<N, 0, false, false>)) \
                   : (which == 1 ? k_expand_thread<N> : k_expand_warp<N>);
         CC_CASES(K1)
 #undef K1
@@ -1455,7 +1614,9 @@ static KernelFn kernel_for(int which, Mode m, int nw, bool pk)
     case 4:
 #define K4(N)                                                                                            \
     if (nw == N)                                                                                         \
-        return bm ? (pk ? k_expand_blocked<N, 3, true> : k_expand_blocked<N, 3, false>) : k_expand_thread<N>;
+        return bm ? (leaf ? (pk ? k_expand_blocked<N, 3, true, true> : k_expand_blocked<N, 3, false, true>)    \
+                          : (pk ? k_expand_blocked<N, 3, true, false> : k_expand_blocked<N, 3, false, false>)) \
+                  : k_expand_thread<N>;
         CC_CASES(K4)
 #undef K4
         break;
@@ -1473,14 +1634,16 @@ cudaError_t launch_wide(int which, const LaunchArgs &a, cudaStream_t st, int gri
 {
     if (a.n_in == 0)
         return cudaSuccess;
-    KernelFn f = which == 0 ? k_stage1_wide : which == 1 ? k_expand_wide : k_shard_filter_wide;
+    KernelFn f = which == 0 ? k_stage1_wide
+                 : which == 1 ? (a.emit && !a.emit_next ? k_expand_wide<true> : k_expand_wide<false>)
+                              : k_shard_filter_wide;
     const u64 per_block = which == 1 ? (u64)(kBlock / 32) * kWidePaths : (u64)kBlock;
     return run(f, grid_for(per_block, a.n_in, grid_cap), 0, st, a);
 }
 
 int max_blocks_per_sm_wide(int which)
 {
-    KernelFn f = which == 0 ? k_stage1_wide : which == 1 ? k_expand_wide : k_shard_filter_wide;
+    KernelFn f = which == 0 ? k_stage1_wide : which == 1 ? k_expand_wide<false> : k_shard_filter_wide;
     int nb = 1;
     if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, (const void *)f, kBlock, 0) != cudaSuccess || nb < 1)
         nb = 1;
@@ -1502,7 +1665,7 @@ cudaError_t launch_expand(const LaunchArgs &a, Mode m, ExpandVariant v, cudaStre
     if (a.n_in == 0)
         return cudaSuccess;
     const int which = v == ExpandVariant::Small ? 4 : (v == ExpandVariant::Thread ? 1 : 2);
-    KernelFn f = kernel_for(which, m, a.g.nw, a.packed != 0);
+    KernelFn f = kernel_for(which, m, a.g.nw, a.packed != 0, a.emit && !a.emit_next);
     if (!f)
         return cudaErrorInvalidValue;
     u64 per_block = kBlock;

@@ -174,6 +174,17 @@ def test_chunked_k50(ws):
     assert_same(got, oracle.enumerate_cycles(*g, nthreads=NT))
 
 
+def test_chunked_gnp_small_workspace(ws):
+    """G(100, 0.1) capped at 9 vertices: |F_7| = 156,775 records do not fit a 1 MB arena, so the
+    deepest-first chunk scheduler must split levels; the result is unchanged."""
+    import torch
+    g = I.gnp(100, 0.1, 4242)
+    small = torch.empty(1 << 20, dtype=torch.uint8, device="cuda")
+    got = binding.enumerate_cycles(*g, workspace=small, max_len=9)
+    assert got["stats"]["chunks"] > 2
+    assert_same(got, oracle.enumerate_cycles(*g, max_len=9, nthreads=NT))
+
+
 def test_workspace_too_small_fails_loudly(ws):
     import torch
     small = torch.empty(64 * 12, dtype=torch.uint8, device="cuda")
@@ -294,14 +305,40 @@ def test_repeat_runs_deterministic(ws):
 
 
 def test_stats_accounting(ws):
-    """Frontier accounting: paths_expanded = sum |F_t|; bytes_alg =
-    record_bytes * (paths read + paths written); t_dev > 0."""
+    """Frontier accounting: paths_expanded = sum |F_t|; with no length cap every
+    path is written once and read once: paths_written = sum_t |F_t| and bytes_alg =
+    record_bytes * (paths read + paths written by the expansions); t_dev > 0."""
     g = I.grid(6, 8)
     r = gpu(g, ws, profile=True)
     s = r["stats"]
     f = r["paths_by_len"]
     assert s["paths_expanded"] == int(f.sum())
+    assert s["paths_written"] == int(f.sum()) and s["leaf_paths"] == 0
     written = int(f[4:].sum())  # every path of >= 4 vertices was written by an expansion
     assert s["bytes_alg"] == s["record_bytes"] * (int(f.sum()) + written)
     assert s["t_dev_ms"] > 0 and s["t_expand_ms"] > 0
     assert s["total_cycles"] == int(r["counts"].sum())
+
+
+@pytest.mark.parametrize("name,g,K", [("grid6x8", I.grid(6, 8), 14), ("gnp100", I.gnp(100, 0.1, 4242), 8),
+                                      ("gnp1200", I.gnp(1200, 0.006, 99), 8)])
+def test_last_level_fusion_accounting(ws, name, g, K):
+    """Count mode with max_len = K (last-level fusion): the paths of K-1 vertices
+    are counted by the launch that creates them and never written; the counts, hash, |F_t| and
+    candidates still equal the oracle's."""
+    r = gpu(g, ws, max_len=K, profile=True)
+    assert_same(r, oracle.enumerate_cycles(*g, max_len=K, nthreads=NT))
+    s = r["stats"]
+    f = r["paths_by_len"]
+    assert s["leaf_paths"] == int(f[K - 1]) > 0
+    assert s["paths_written"] == int(f[3:K - 1].sum())
+
+
+def test_collect_mode_writes_every_path(ws):
+    """Collect mode (S records) has no last-level fusion: every created path is written."""
+    g = I.grid(5, 6)
+    r = gpu(g, ws, collect=True, max_len=10)
+    s = r["stats"]
+    f = r["paths_by_len"]
+    assert s["leaf_paths"] == 0
+    assert s["paths_written"] == int(f.sum())
