@@ -81,7 +81,13 @@ typedef struct {
                                  required capacity in the message and in cc_stats */
     uint32_t profile;         /* 1 = time every expansion launch with CUDA events
                                  (cc_stats.t_expand_ms); 0 = only the total */
-    uint32_t min_shard_paths; /* paths per shard before sharding (0 = 1024) */
+    uint32_t min_shard_paths; /* shard_count > 1: the first frontier level with at least
+                                 min_shard_paths * shard_count paths is partitioned (0 = 2^20);
+                                 Stage 1 is partitioned instead when it has at least that many
+                                 forward pairs (0 = 2^16 per shard).  The partition is a function
+                                 of the graph, shard_count and min_shard_paths -- and, only when an
+                                 unsharded level does not fit the arena, of the arena size: give
+                                 every rank the same workspace_bytes */
 } cc_options;
 
 /* Statistics of one cc_enumerate call (cc_result_stats). */

@@ -438,6 +438,7 @@ struct Level {
     bool sharded = false;   // paths already partitioned between shards (owned by this one)
     bool init = false;      // sharded flag fixed (at the level's first write)
     double fan = 0;         // observed extensions per path at this level (0 = unknown)
+    bool shard_now = false; // unsharded level whose expansion does not fit: partition it first
 };
 
 }  // namespace
@@ -604,7 +605,13 @@ static cc_status enumerate_impl(const cc_graph *cg, const cc_options *opt_in, cc
     const int grid_sf = (wide ? cc::max_blocks_per_sm_wide(2) : cc::max_blocks_per_sm(3, mode, nw, packed, 0)) * sms;
     const double maxfan = (double)std::max<int64_t>(g->max_deg - 1, 1);
     const uint32_t W = opt.shard_count;
-    const u64 shard_threshold = (u64)(opt.min_shard_paths ? opt.min_shard_paths : 1024) * W;
+    // Multi-GPU partition: the first frontier level with >= threshold paths is
+    // split by content hash.  Deep enough that the heavy-tailed subtree sizes average out (P10x10
+    // at W = 8: max/mean shard time 1.37 at 1024 paths per shard, 1.01 at 2^20 -- measured,
+    // profiles/), while the levels above it (expanded redundantly by every rank) stay small.
+    // Stage 1 is split instead when its pair space alone is large (e.g. K_{150,150}).
+    const u64 shard_threshold = (u64)(opt.min_shard_paths ? opt.min_shard_paths : (1u << 20)) * W;
+    const u64 s1_shard_threshold = (u64)(opt.min_shard_paths ? opt.min_shard_paths : (1u << 16)) * W;
     const uint32_t max_len = opt.max_len;
     const bool want_paths = max_len == 0 || max_len >= 4;
 
@@ -733,7 +740,7 @@ static cc_status enumerate_impl(const cc_graph *cg, const cc_options *opt_in, cc
     S.stage1_pairs = stage1_total;
     u64 s1_next = 0;
     // shard at Stage 1 when the seed space alone is large enough (deterministic: graph-only)
-    const bool s1_filter = W > 1 && stage1_total >= shard_threshold;
+    const bool s1_filter = W > 1 && stage1_total >= s1_shard_threshold;
     levels[3].init = true;
     levels[3].sharded = W == 1 || s1_filter;
     int deepest = 2;  // levels 3..deepest may be non-empty
@@ -771,7 +778,7 @@ static cc_status enumerate_impl(const cc_graph *cg, const cc_options *opt_in, cc
         const int d = deepest;
         Level &L = levels[d];
         // ---- multi-GPU: partition the first frontier level with >= threshold paths
-        if (W > 1 && !L.sharded && L.count >= shard_threshold) {
+        if (W > 1 && !L.sharded && (L.count >= shard_threshold || L.shard_now)) {
             bool of = false;
             trace_level = d;
             cc_status s = launch(FILTER, L.pages.data(), L.pages.size(), L.count, 0, true, false, false, false, used,
@@ -831,9 +838,12 @@ static cc_status enumerate_impl(const cc_graph *cg, const cc_options *opt_in, cc
             if (s != CC_OK)
                 return s;
             if (of) {
-                if (W > 1 && !L.sharded)
-                    return fail(CC_ERR_CAPACITY, "workspace too small to expand the unsharded level F_" +
-                                                     std::to_string(d) + " whole (needed before sharding)");
+                if (W > 1 && !L.sharded) {
+                    // an unsharded level is expanded whole; if its children do not fit, shard it
+                    // now (the decision is still a function of the graph only)
+                    L.shard_now = true;
+                    break;
+                }
                 if (k == 1)
                     return fail(CC_ERR_CAPACITY, "workspace too small: one page of F_" + std::to_string(d) +
                                                      " needs " + std::to_string(h_sc->out_count) +

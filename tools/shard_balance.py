@@ -59,7 +59,7 @@ for w in a.shards:
             paths.append(int(s["paths_expanded"]))
             ms.append(float(s["t_dev_ms"]))
         print(json.dumps({
-            "workload": a.workload, "W": w, "min_shard_paths": msp or 1024,
+            "workload": a.workload, "W": w, "min_shard_paths": msp or "default",
             "exact": bool((tot == c0).all() and hs == h0),
             "paths": paths, "t_dev_ms": [round(x, 2) for x in ms],
             "paths_max_over_mean": max(paths) / (sum(paths) / w),
