@@ -561,6 +561,7 @@ __global__ void __launch_bounds__(kBlock, NW <= 2 ? 3 : 2) k_expand_blocked(cons
 
     const uint32_t idb = PACK ? p.idb : (uint32_t)kIdBits;
     const uint32_t idm = (1u << idb) - 1;
+    const u64 keep_v12 = PACK ? ~((u64)idm << (64 - idb)) : ~0ull;  // packed: vt field cleared
     const u64 n_tiles = (p.n_in + kTile - 1) / kTile;
     const u64 my_tiles = blockIdx.x < n_tiles ? (n_tiles - 1 - blockIdx.x) / gridDim.x + 1 : 0;
     // tile k of this CTA -> global tile blockIdx.x + k * gridDim.x -> its page and slot
@@ -587,20 +588,28 @@ __global__ void __launch_bounds__(kBlock, NW <= 2 ? 3 : 2) k_expand_blocked(cons
         for (u64 k = 0; k < my_tiles && k < (u64)kStages; ++k)
             issue(k);
     }
+    // closed rows N[v] = Adj(v) | {v} in s_adj: vt and v1 always lie in B, so Cand/Close/Ext are
+    // unchanged, and the children's blocked set B | N[vt] is a plain OR
     for (int i = threadIdx.x; i < p.g.n * NW; i += kBlock) {
-        const int sh = i / NW + 1 - 64 * (i % NW);
-        s_above[i] = sh <= 0 ? ~0ull : (sh >= 64 ? 0ull : (~0ull << sh));
+        s_above[i] = above_word((uint32_t)(i / NW), i % NW);
+        s_adj[i] = p.g.adj[i] | bit_in_word(i % NW, (uint32_t)(i / NW));
     }
-    stage_graph<NW, false>(p.g, s_adj, s_key, nullptr);  // includes __syncthreads
+    for (int i = threadIdx.x; i < p.g.n; i += kBlock)
+        s_key[i] = p.g.key[i];
+    __syncthreads();
 
-    u64 cnt = 0, hs = 0, cand = 0;
-    u64 leaf_paths = 0, leaf_cand = 0, leaf_cyc = 0;
+    // per-thread statistics in 32 bits (a launch gives a thread at most ~10^5 paths, n <= 512)
+    uint32_t cnt = 0, cand = 0;
+    u64 hs = 0;
+    uint32_t leaf_paths = 0, leaf_cand = 0, leaf_cyc = 0;
+    const u64 pmask = (1ull << p.pg.log_p) - 1;
     // last level (p.emit && !p.emit_next): the children <p,v> cannot have children within the
     // length cap; they are counted -- |F_{t+1}|, deg(v), their closures -- and not written
     constexpr bool leaf = LEAF;  // launched iff p.emit && !p.emit_next
     for (u64 k = 0; k < my_tiles; ++k) {
         const int st = (int)(k % kStages);
         const u64 base = (blockIdx.x + k * gridDim.x) * (u64)kTile;
+        const bool full = base + kTile <= p.n_in;
         mbar_wait(&bar[st], (uint32_t)((k / kStages) & 1));
         const char *buf = ring + (size_t)st * kStageBytes;
         u64 W[R][RW];
@@ -612,7 +621,7 @@ __global__ void __launch_bounds__(kBlock, NW <= 2 ? 3 : 2) k_expand_blocked(cons
 #pragma unroll
             for (int w = 0; w < RW; ++w)
                 W[i][w] = ((const u64 *)buf)[w * kTile + j];
-            valid[i] = base + j < p.n_in;
+            valid[i] = full || base + j < p.n_in;
             id[i] = PACK ? packed_ids(W[i][NW - 1], idb) : ((const uint32_t *)(buf + (size_t)RW * kTile * 8))[j];
         }
         u64 ext[R][NW];
@@ -632,10 +641,11 @@ __global__ void __launch_bounds__(kBlock, NW <= 2 ? 3 : 2) k_expand_blocked(cons
             lds_row<NW>(s_adj, vt, arow);
             lds_row<NW>(s_above, v2, abv);
             lds_row<NW>(s_adj, v1, a1row);
+            cand -= 1;  // deg(vt) = |N[vt]| - 1: the candidate slots of Alg. 3 (statistic)
 #pragma unroll
             for (int w = 0; w < NW; ++w) {
                 const u64 a = arow[w];
-                cand += __popcll(a);  // deg(vt): the candidate slots of Alg. 3 (statistic)
+                cand += __popcll(a);
                 // the packed ids sit above bit n, where a is zero: they never leak into c
                 const u64 c = a & abv[w] & ~W[i][w];
                 const u64 a1 = a1row[w];
@@ -662,7 +672,7 @@ __global__ void __launch_bounds__(kBlock, NW <= 2 ? 3 : 2) k_expand_blocked(cons
                 u64 Z[NW];
 #pragma unroll
                 for (int w = 0; w < NW; ++w) {
-                    Z[w] = abv[w] & ~(W[i][w] | arow[w] | bit_in_word(w, vt)) & a1row[w];
+                    Z[w] = abv[w] & ~(W[i][w] | arow[w]) & a1row[w];  // v is in B | N[vt]
                     ne -= __popcll(ext[i][w]);
                 }
                 if (p.count) {
@@ -677,6 +687,7 @@ __global__ void __launch_bounds__(kBlock, NW <= 2 ? 3 : 2) k_expand_blocked(cons
                             lds_row<NW>(s_adj, v, av);
                             const u64 ksv = W[i][NW] + s_key[v];
                             leaf_paths++;
+                            leaf_cand -= 1;  // closed row
 #pragma unroll
                             for (int w2 = 0; w2 < NW; ++w2) {
                                 leaf_cand += __popcll(av[w2]);
@@ -724,7 +735,7 @@ __global__ void __launch_bounds__(kBlock, NW <= 2 ? 3 : 2) k_expand_blocked(cons
                 lds_row<NW>(s_adj, vt, ar);
 #pragma unroll
                 for (int w = 0; w < NW; ++w)
-                    s_par[slot * PW + w] = W[i][w] | ar[w] | bit_in_word(w, vt);
+                    s_par[slot * PW + w] = W[i][w] | ar[w];  // B | N[vt]
                 s_par[slot * PW + NW] = W[i][NW];
                 if (!PACK)
                     s_pid[slot] = id[i] & ((1u << (2 * idb)) - 1);
@@ -778,7 +789,7 @@ __global__ void __launch_bounds__(kBlock, NW <= 2 ? 3 : 2) k_expand_blocked(cons
                     u64 C[RW];
 #pragma unroll
                     for (int w = 0; w < NW; ++w)
-                        C[w] = W[i][w] | s_adj[vt * NW + w] | bit_in_word(w, vt);
+                        C[w] = W[i][w] | s_adj[vt * NW + w];
 #pragma unroll
                     for (int w = 0; w < NW; ++w) {
                         u64 m = ext[i][w];
@@ -798,6 +809,12 @@ __global__ void __launch_bounds__(kBlock, NW <= 2 ? 3 : 2) k_expand_blocked(cons
                 }
             }
         } else if (tile_base + total <= p.out_cap) {
+            // output positions o0 + j: page pg0 from slot s0 up to `split`, then page pg0 + 1
+            const u64 o0 = p.out_off + tile_base;
+            const uint32_t s0 = (uint32_t)(o0 & pmask);
+            const uint32_t split = (uint32_t)(pmask + 1 - s0);
+            char *pp0 = page_ptr(p.pg, p.pg.out_pages[o0 >> p.pg.log_p]);
+            char *pp1 = split < total ? page_ptr(p.pg, p.pg.out_pages[(o0 >> p.pg.log_p) + 1]) : pp0;
             for (unsigned int j = threadIdx.x; j < total; j += kBlock) {
                 const uint32_t e = s_child[j];
                 const uint32_t slot = e & 0xffffu;
@@ -835,14 +852,19 @@ __global__ void __launch_bounds__(kBlock, NW <= 2 ? 3 : 2) k_expand_blocked(cons
                 for (int w = 0; w < NW; ++w)
                     C[w] = par[w];
                 C[NW] = par[NW] + s_key[v];
+                const bool lo = j < split;
+                char *pp = lo ? pp0 : pp1;
+                const uint32_t oslot = lo ? s0 + j : j - split;
+                u64 *w0 = (u64 *)pp + oslot;
                 if (PACK) {
-                    // child ids: (v1, v2) of the parent, last vertex v
-                    const uint32_t v12 = packed_ids(C[NW - 1], idb) & ((1u << (2 * idb)) - 1);
-                    C[NW - 1] = with_packed_ids(C[NW - 1], v12 | (v << (2 * idb)), idb);
-                    store_record<RW, false>(p.pg, p.out_off + tile_base + j, C, 0);
+                    // child ids: (v1, v2) of the parent, last vertex v (the top idb bits)
+                    C[NW - 1] = (C[NW - 1] & keep_v12) | ((u64)v << (64 - idb));
                 } else {
-                    store_record<RW, true>(p.pg, p.out_off + tile_base + j, C, s_pid[slot] | (v << (2 * idb)));
+                    ((uint32_t *)(pp + ((u64)RW << p.pg.log_p) * 8))[oslot] = s_pid[slot] | (v << (2 * idb));
                 }
+#pragma unroll
+                for (int w = 0; w < RW; ++w)
+                    w0[(size_t)w << p.pg.log_p] = C[w];
             }
         }
     }
