@@ -46,6 +46,16 @@ WORKLOADS = {
 }
 DEFAULT_WORKLOAD = "p10x10"
 
+# Integer-ALU roofline (K_{a,b}): issue-bound peak = 148 SMs x 4 SMSPs x 32 lanes x
+# 1.965 GHz (one warp instruction per SMSP per clock; B200_PROFILING.md, B300_MICROARCH.md pipe
+# rates); the algorithmic work per cycle is the H-spec hash mix(keysum + key(w)) (two 64-bit
+# multiplies and three xor-shifts on 32-bit lanes ~ 20 lane-ops, plus the add and the bit
+# extraction ~ 4) and per candidate slot one bit test of the word-parallel candidate scan (~1)
+ALU_BOUND = {"k150"}
+ALU_PEAK_LANE_OPS = 148 * 4 * 32 * 1.965e9
+ALU_OPS_PER_CYCLE = 24
+ALU_OPS_PER_SLOT = 1
+
 # oracle samples (bounded CPU work, ~10-30 s) for cpu_baseline / --impl reference
 ORACLE_SAMPLE = {
     "p10x10": dict(max_len=31),
@@ -288,6 +298,18 @@ def main():
                 "peak_kind": peak_kind,
                 "kernel": "k_expand_blocked" if g[0] <= 512 else "k_expand_wide", "expand_share_of_step": t_expand / dev_ms if dev_ms else None,
                 "bytes_alg_per_step": bytes_alg / args.steps}
+    if args.workload in ALU_BOUND:
+        # K_{a,b}: one expansion round in which every gate-passing candidate closes; no frontier
+        # is written, so HBM is idle and the path is integer-ALU bound: the
+        # algorithmic work is the H-spec hash of every cycle plus the candidate-slot tests
+        t_all = sum(s["t_expand_ms"] + s["t_stage1_ms"] for s in stats) / args.steps
+        ops = (ALU_OPS_PER_CYCLE * cycles_total / world + ALU_OPS_PER_SLOT * st_last["candidates"])
+        alu_peak = ALU_PEAK_LANE_OPS  # issue-bound integer peak, DESIGN.md §6
+        ach = ops / (t_all / 1e3) if t_all > 0 else 0.0
+        roofline = {"bound": "alu", "achieved": ach / 1e12, "peak": alu_peak / 1e12, "unit": "Tlane-op/s",
+                    "frac": ach / alu_peak, "traffic": None, "peak_kind": "derived (DESIGN.md §6)",
+                    "kernel": "k_stage1 + k_expand_blocked", "ops_per_step": ops,
+                    "expand_share_of_step": t_all / ms_per_step if ms_per_step else None}
 
     # ---- end to end through the public API with host buffers (labelling + upload + D2H)
     e2e = None

@@ -306,7 +306,10 @@ static cc_status ensure_device_graph(cc_graph *g, int device, u64 seed, cudaStre
                      s_adj = align_up(std::max<size_t>(g->adj.size(), 1) * 8, 256),
                      s_orig = align_up(std::max<int64_t>(n, 1) * 4, 256), s_key = align_up(std::max<int64_t>(n, 1) * 8, 256),
                      s_kb = g->nw <= cc::kByteTableWords ? align_up((size_t)8 * g->nw * 256 * 8, 256) : 256;
-        dc->bytes = s_row + s_col + s_fwd + s_pp + s_adj + s_orig + s_key + s_kb;
+        // wide sparse graphs: the neighbour-mask table of the last-level fusion (cc_internal.h)
+        const bool want_nm = g->wide && g->max_deg <= 32;
+        const size_t s_nm = want_nm ? align_up((size_t)n * n * 4, 256) : 0;
+        dc->bytes = s_row + s_col + s_fwd + s_pp + s_adj + s_orig + s_key + s_kb + s_nm;
         CC_CUDA(cudaMalloc(&dc->buf, dc->bytes));
         char *p = (char *)dc->buf;
         auto *rowptr = (uint32_t *)p; p += s_row;
@@ -316,7 +319,8 @@ static cc_status ensure_device_graph(cc_graph *g, int device, u64 seed, cudaStre
         auto *adj = (u64 *)p; p += s_adj;
         auto *orig = (int32_t *)p; p += s_orig;
         auto *key = (u64 *)p; p += s_key;
-        auto *keybyte = (u64 *)p;
+        auto *keybyte = (u64 *)p; p += s_kb;
+        auto *nbrmask = want_nm ? (uint32_t *)p : nullptr;
         CC_CUDA(cudaMemcpyAsync(rowptr, g->irow.data(), (n + 1) * 4, cudaMemcpyHostToDevice, st));
         if (!g->icol.empty())
             CC_CUDA(cudaMemcpyAsync(col, g->icol.data(), g->icol.size() * 4, cudaMemcpyHostToDevice, st));
@@ -338,6 +342,11 @@ static cc_status ensure_device_graph(cc_graph *g, int device, u64 seed, cudaStre
         dc->dg.key = key;
         dc->dg.keybyte = keybyte;
         dc->dg.orig = orig;
+        dc->dg.nbrmask = nbrmask;
+        if (nbrmask) {
+            CC_CUDA(cudaMemsetAsync(nbrmask, 0, (size_t)n * n * 4, st));
+            CC_CUDA(cc::launch_nbrmask(dc->dg, nbrmask, st));
+        }
     }
     if (!dc->keys_valid || dc->key_seed != seed) {
         CC_CUDA(cc::launch_keys((u64 *)dc->dg.key, (u64 *)dc->dg.keybyte, dc->dg.orig, (int)n, g->nw, seed, st));

@@ -34,6 +34,8 @@ struct DevGraph {
     const u64 *keybyte;          // [8*nw][256] (nw <= 2): sum of key(8j+i) over the set bits i of
                                  //        byte value b at byte position j of S
     const int32_t *orig;         // [n]    internal id -> original id
+    const uint32_t *nbrmask;     // wide class with Delta <= 32, else null: [n][n], bit k of
+                                 //        nbrmask[u*n + z] = (k-th neighbour of u in its CSR row) ~ z
 };
 
 // Two record formats ("modes") for a path p = <v1..vt>:
@@ -131,6 +133,8 @@ cudaError_t launch_expand(const LaunchArgs &a, Mode m, ExpandVariant v, cudaStre
 cudaError_t launch_shard_filter(const LaunchArgs &a, Mode m, cudaStream_t st, int grid_cap);
 cudaError_t launch_keys(u64 *key, u64 *keybyte, const int32_t *orig, int n, int nw, u64 seed,
                         cudaStream_t st);
+// nbrmask (DevGraph) of a wide graph with Delta <= 32; T must be zeroed, n*n words
+cudaError_t launch_nbrmask(const DevGraph &g, uint32_t *T, cudaStream_t st);
 cudaError_t launch_cycle_lengths(const CycleStore &c, int nw, uint64_t first, uint64_t count,
                                  uint32_t *len, cudaStream_t st);
 cudaError_t launch_cycle_sequences(const CycleStore &c, int nw, const u64 *adj, const int32_t *orig,

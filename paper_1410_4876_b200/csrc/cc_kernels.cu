@@ -605,7 +605,6 @@ __global__ void __launch_bounds__(kBlock, NW <= 2 ? 3 : 2) k_expand_blocked(cons
     const u64 pmask = (1ull << p.pg.log_p) - 1;
     // last level (p.emit && !p.emit_next): the children <p,v> cannot have children within the
     // length cap; they are counted -- |F_{t+1}|, deg(v), their closures -- and not written
-    constexpr bool leaf = LEAF;  // launched iff p.emit && !p.emit_next
     for (u64 k = 0; k < my_tiles; ++k) {
         const int st = (int)(k % kStages);
         const u64 base = (blockIdx.x + k * gridDim.x) * (u64)kTile;
@@ -1209,14 +1208,11 @@ __global__ void __launch_bounds__(kBlock) k_stage1_wide(const LaunchArgs p)
 constexpr int kWidePaths = 4;  // paths per warp per tile in k_expand_wide
 
 constexpr int kWideVList = 256;  // child-vertex list per warp (children of one path)
-constexpr int kWideZList = 32;   // closer list Z(p) per warp (last-level fusion)
 
-template <bool LEAF>
 __global__ void __launch_bounds__(kBlock) k_expand_wide(const LaunchArgs p)
 {
     __shared__ ReserveSmem rs;
     __shared__ uint32_t s_vlist[(kBlock / 32) * kWideVList];
-    __shared__ uint32_t s_zlist[(kBlock / 32) * kWideZList];
     const int NW = p.g.nw, RW = NW + 1;
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
     const uint32_t idb = p.idb, idm = (1u << idb) - 1;
@@ -1224,14 +1220,7 @@ __global__ void __launch_bounds__(kBlock) k_expand_wide(const LaunchArgs p)
     const u64 *__restrict__ key = p.g.key;
     const bool mine = lane < NW;  // this lane owns word `lane` of every record
     constexpr u64 kTilePaths = (u64)(kBlock / 32) * kWidePaths;
-    // last level (p.emit && !p.emit_next): the children are counted, not written (see
-    // k_expand_blocked); their closures Adj(v) & Z(p) are found by probing the few closers z in
-    // Z(p) (a list in shared memory) against row v, one bit test each
-    constexpr bool leaf = LEAF;  // launched iff p.emit && !p.emit_next
-    uint32_t *sv = s_vlist + wid * kWideVList;
-    uint32_t *sz = s_zlist + wid * kWideZList;
     u64 cnt = 0, hs = 0, cand = 0;
-    u64 leaf_paths = 0, leaf_cand = 0, leaf_cyc = 0;
     for (u64 tb = (u64)blockIdx.x * kTilePaths; tb < p.n_in; tb += (u64)gridDim.x * kTilePaths) {
         u64 ext[kWidePaths], Cw[kWidePaths], ksv[kWidePaths];
         u64 v12v[kWidePaths], Bv[kWidePaths], KSv[kWidePaths];
@@ -1276,94 +1265,11 @@ __global__ void __launch_bounds__(kBlock) k_expand_wide(const LaunchArgs p)
                     hs += mix64(ks + __ldg(key + 64 * lane + b));
                 }
             }
-            const unsigned int E = __reduce_add_sync(FULL_MASK, (unsigned int)__popcll(ext[i]));
+            ne += __reduce_add_sync(FULL_MASK, (unsigned int)__popcll(ext[i]));
             // the children's blocked set: vt becomes interior -> B | N[vt]
             Cw[i] = mine ? (B | a | bit_in_word(lane, vt)) : 0ull;
             ksv[i] = ks;
             v12v[i] = id & ((1ull << (2 * idb)) - 1);
-            if constexpr (!LEAF) {
-                ne += E;
-            } else if (E && p.count) {
-                const u64 Zw = mine ? (above_word(v2, lane) & ~Cw[i] & a1) : 0ull;
-                const unsigned int pz = __popcll(Zw);
-                unsigned int zincl = pz;
-#pragma unroll
-                for (int d = 1; d < 32; d <<= 1) {
-                    const unsigned int t = __shfl_up_sync(FULL_MASK, zincl, d);
-                    if (lane >= d)
-                        zincl += t;
-                }
-                const unsigned int nz = __shfl_sync(FULL_MASK, zincl, 31);
-                if (nz <= (unsigned int)kWideZList) {
-                    u64 m = Zw;
-                    unsigned int pos = zincl - pz;
-                    while (m) {
-                        const int b = __ffsll((long long)m) - 1;
-                        m &= m - 1;
-                        sz[pos++] = (uint32_t)(64 * lane + b);
-                    }
-                }
-                // the children in batches that fit the vertex list: all lanes, or 8 groups of
-                // 4 lanes (a lane holds at most 64 children)
-                const int ngroups = E <= (unsigned int)kWideVList ? 1 : 8;
-                for (int gi = 0; gi < ngroups; ++gi) {
-                    const bool inb = ngroups == 1 || (lane >> 2) == gi;
-                    const uint32_t pc = inb ? __popcll(ext[i]) : 0u;
-                    unsigned int incl = pc;
-#pragma unroll
-                    for (int d = 1; d < 32; d <<= 1) {
-                        const unsigned int t = __shfl_up_sync(FULL_MASK, incl, d);
-                        if (lane >= d)
-                            incl += t;
-                    }
-                    const unsigned int Eb = __shfl_sync(FULL_MASK, incl, 31);
-                    if (Eb == 0)
-                        continue;
-                    if (inb) {
-                        u64 m = ext[i];
-                        unsigned int pos = incl - pc;
-                        while (m) {
-                            const int b = __ffsll((long long)m) - 1;
-                            m &= m - 1;
-                            sv[pos++] = (uint32_t)(64 * lane + b);
-                        }
-                    }
-                    __syncwarp();
-                    if (lane == 0)
-                        leaf_paths += Eb;
-                    for (unsigned int e = lane; e < Eb; e += 32) {
-                        const uint32_t v = sv[e];
-                        leaf_cand += __ldg(p.g.rowptr + v + 1) - __ldg(p.g.rowptr + v);
-                    }
-                    if (nz <= (unsigned int)kWideZList) {
-                        for (unsigned int e = lane; e < Eb; e += 32) {
-                            const uint32_t v = sv[e];
-                            const u64 kv = ks + __ldg(key + v);
-                            const u64 *row = adj + (u64)v * NW;
-                            for (unsigned int q = 0; q < nz; ++q) {
-                                const uint32_t z = sz[q];
-                                if ((__ldg(row + (z >> 6)) >> (z & 63)) & 1ull) {
-                                    leaf_cyc++;
-                                    hs += mix64(kv + __ldg(key + z));
-                                }
-                            }
-                        }
-                    } else {
-                        for (unsigned int e = 0; e < Eb; ++e) {
-                            const uint32_t v = sv[e];
-                            u64 cl = mine ? (__ldg(adj + (u64)v * NW + lane) & Zw) : 0ull;
-                            leaf_cyc += __popcll(cl);
-                            const u64 kv = ks + __ldg(key + v);
-                            while (cl) {
-                                const int b = __ffsll((long long)cl) - 1;
-                                cl &= cl - 1;
-                                hs += mix64(kv + __ldg(key + 64 * lane + b));
-                            }
-                        }
-                    }
-                    __syncwarp();
-                }
-            }
         }
         // one reservation per CTA tile; the warp's count is carried by its lane 0
         const u64 off = __shfl_sync(FULL_MASK, block_reserve(lane == 0 ? ne : 0u, &p.sc->out_count, rs), 0);
@@ -1452,13 +1358,262 @@ __global__ void __launch_bounds__(kBlock) k_expand_wide(const LaunchArgs p)
     }
     if (!p.count)
         cand = 0;
+    flush_accum(cnt, hs, cand, p.sc);
+}
+
+// Last-level fusion for the wide class (p.emit && !p.emit_next, see Scratch): F_t is read and
+// its own closures counted as in k_expand_wide; its children <p,v> (v in Ext(p)) are counted
+// and their closures found, but nothing is written.  Close(<p,v>) = Adj(v) & Z(p), counted the
+// other way round: for each closer z in Z(p) = {x > v2} & ~(B | N[vt]) & Adj(v1) (few: inside
+// Adj(v1)), one coalesced read of row z, AND Ext(p), gives every child closing through z.
+// Latency-bound code, so the work is phased: one warp takes kLeafPaths paths, issues all their
+// row reads before using any, then lists every (path, z) pair and reads those rows in batches.
+// No block-level synchronisation: warps run independently.
+constexpr int kLeafPaths = 4;
+constexpr int kLeafPairs = 128;  // (path, closer) pairs listed per warp and round
+constexpr int kLeafBatch = 8;    // closer rows in flight per lane
+
+__global__ void __launch_bounds__(kBlock) k_leaf_wide(const LaunchArgs p)
+{
+    __shared__ uint16_t s_deg[2048];  // deg(v), n <= 2015
+    __shared__ uint32_t s_pair[(kBlock / 32) * kLeafPairs];
+    const int NW = p.g.nw, RW = NW + 1;
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    const uint32_t idb = p.idb, idm = (1u << idb) - 1;
+    const u64 *__restrict__ adj = p.g.adj;
+    const u64 *__restrict__ key = p.g.key;
+    const bool mine = lane < NW;  // this lane owns word `lane` of every row / record
+    for (int v = threadIdx.x; v < p.g.n; v += kBlock)
+        s_deg[v] = (uint16_t)(p.g.rowptr[v + 1] - p.g.rowptr[v]);
+    __syncthreads();
+    uint32_t *pair = s_pair + wid * kLeafPairs;
+    const bool nbm = p.g.nbrmask != nullptr;
+    u64 cnt = 0, hs = 0, cand = 0, lpaths = 0, lcand = 0, lcyc = 0;
+    const u64 nwarps = (u64)gridDim.x * (kBlock / 32);
+    for (u64 r0 = ((u64)blockIdx.x * (kBlock / 32) + wid) * kLeafPaths; r0 < p.n_in; r0 += nwarps * kLeafPaths) {
+        u64 B[kLeafPaths], KS[kLeafPaths], a[kLeafPaths], a1[kLeafPaths];
+        uint32_t v2v[kLeafPaths], vtv[kLeafPaths];
+        // phase A: the records
+#pragma unroll
+        for (int i = 0; i < kLeafPaths; ++i) {
+            B[i] = 0;
+            KS[i] = 0;
+            if (r0 + i < p.n_in) {
+                const u64 *rec = wide_rec(p.pg, p.pg.in_pages, r0 + i, RW);
+                B[i] = mine ? rec[lane] : 0ull;
+                KS[i] = lane == 0 ? rec[NW] : 0ull;
+            }
+        }
+        // phase B: rows Adj(vt), Adj(v1) of every path, all in flight together
+#pragma unroll
+        for (int i = 0; i < kLeafPaths; ++i) {
+            KS[i] = __shfl_sync(FULL_MASK, KS[i], 0);
+            const u64 id = packed_ids(__shfl_sync(FULL_MASK, B[i], NW - 1), idb);
+            const uint32_t v1 = (uint32_t)(id & idm);
+            v2v[i] = (uint32_t)((id >> idb) & idm);
+            vtv[i] = (uint32_t)(id >> (2 * idb));
+            const bool ok = r0 + i < p.n_in && mine;
+            a[i] = ok ? __ldg(adj + (u64)vtv[i] * NW + lane) : 0ull;
+            a1[i] = ok ? __ldg(adj + (u64)v1 * NW + lane) : 0ull;
+        }
+        // phase C: Cand/Close/Ext of each path (its own closures: cycles of t+1 vertices), the
+        // children's statistics, and the (path, closer) pair list
+        u64 ext[kLeafPaths];
+        uint32_t extm[kLeafPaths], rowb[kLeafPaths];  // mask path: Ext(p) over the CSR row of vt
+        unsigned int np = 0;
+#pragma unroll
+        for (int i = 0; i < kLeafPaths; ++i) {
+            const u64 abv = above_word(v2v[i], lane);
+            const u64 c = a[i] & abv & ~B[i];
+            u64 close = c & a1[i];
+            ext[i] = c & ~a1[i];
+            if (p.count) {
+                cand += __popcll(a[i]);
+                cnt += __popcll(close);
+                while (close) {
+                    const int b = __ffsll((long long)close) - 1;
+                    close &= close - 1;
+                    hs += mix64(KS[i] + __ldg(key + 64 * lane + b));
+                }
+                if (!nbm) {
+                    u64 m = ext[i];
+                    lpaths += __popcll(m);
+                    while (m) {  // candidate slots of the children: deg(v)
+                        const int b = __ffsll((long long)m) - 1;
+                        m &= m - 1;
+                        lcand += s_deg[64 * lane + b];
+                    }
+                }
+            }
+            if (nbm) {
+                // Ext(p) as a mask over the CSR row of vt: lane k tests its neighbour v_k
+                rowb[i] = p.g.rowptr[vtv[i]];
+                const uint32_t dt = s_deg[vtv[i]];
+                const uint32_t vk = (uint32_t)lane < dt ? p.g.col[rowb[i] + lane] : 0u;
+                const u64 wv = __shfl_sync(FULL_MASK, ext[i], (int)(vk >> 6));
+                const bool eb = (uint32_t)lane < dt && ((wv >> (vk & 63)) & 1ull);
+                extm[i] = __ballot_sync(FULL_MASK, eb);
+                if (p.count) {
+                    lpaths += eb ? 1u : 0u;
+                    lcand += eb ? s_deg[vk] : 0u;
+                }
+            } else {
+                extm[i] = 0;
+                rowb[i] = 0;
+            }
+            const bool anyext = __any_sync(FULL_MASK, ext[i] != 0ull);
+            // Z(p) = {x > v2} & ~(B | N[vt]) & Adj(v1), vt in B
+            u64 zm = (anyext && mine) ? (abv & ~(B[i] | a[i]) & a1[i]) : 0ull;
+            const unsigned int pz = __popcll(zm);
+            unsigned int incl = pz;
+#pragma unroll
+            for (int d = 1; d < 32; d <<= 1) {
+                const unsigned int t = __shfl_up_sync(FULL_MASK, incl, d);
+                if (lane >= d)
+                    incl += t;
+            }
+            unsigned int pos = np + incl - pz;
+            while (zm) {
+                const int b = __ffsll((long long)zm) - 1;
+                zm &= zm - 1;
+                if (pos < (unsigned int)kLeafPairs)
+                    pair[pos] = ((uint32_t)i << 12) | (uint32_t)(64 * lane + b);
+                ++pos;
+            }
+            np += __shfl_sync(FULL_MASK, incl, 31);
+        }
+        __syncwarp();
+        if (p.count && nbm) {
+            // phase D (Delta <= 32): lane-parallel over the (path, z) pairs; the children of p
+            // closing through z are nbrmask[vt][z] & Ext(p), one 4-byte read per pair
+            for (unsigned int q0 = 0; q0 < np; q0 += kLeafPairs) {
+                if (q0 > 0) {
+                    // (rare) more pairs than the list holds: rebuild the next window
+                    __syncwarp();
+                    unsigned int seen = 0;
+#pragma unroll
+                    for (int i = 0; i < kLeafPaths; ++i) {
+                        const bool anyext = __any_sync(FULL_MASK, ext[i] != 0ull);
+                        u64 zm = (anyext && mine) ? (above_word(v2v[i], lane) & ~(B[i] | a[i]) & a1[i]) : 0ull;
+                        const unsigned int pz = __popcll(zm);
+                        unsigned int incl = pz;
+#pragma unroll
+                        for (int d = 1; d < 32; d <<= 1) {
+                            const unsigned int t = __shfl_up_sync(FULL_MASK, incl, d);
+                            if (lane >= d)
+                                incl += t;
+                        }
+                        unsigned int pos = seen + incl - pz;
+                        while (zm) {
+                            const int b = __ffsll((long long)zm) - 1;
+                            zm &= zm - 1;
+                            if (pos >= q0 && pos < q0 + kLeafPairs)
+                                pair[pos - q0] = ((uint32_t)i << 12) | (uint32_t)(64 * lane + b);
+                            ++pos;
+                        }
+                        seen += __shfl_sync(FULL_MASK, incl, 31);
+                    }
+                    __syncwarp();
+                }
+                const unsigned int nq = min(np - q0, (unsigned int)kLeafPairs);
+                for (unsigned int q = lane; q < nq; q += 32) {
+                    const uint32_t e = pair[q];
+                    const uint32_t i = e >> 12, z = e & 0xfffu;
+                    uint32_t em = extm[0], vt = vtv[0], rb = rowb[0];
+                    u64 ks = KS[0];
+#pragma unroll
+                    for (int j = 1; j < kLeafPaths; ++j) {
+                        em = i == (uint32_t)j ? extm[j] : em;
+                        vt = i == (uint32_t)j ? vtv[j] : vt;
+                        rb = i == (uint32_t)j ? rowb[j] : rb;
+                        ks = i == (uint32_t)j ? KS[j] : ks;
+                    }
+                    uint32_t m = __ldg(p.g.nbrmask + (u64)vt * p.g.n + z) & em;
+                    if (m) {
+                        lcyc += __popc(m);
+                        const u64 kz = ks + __ldg(key + z);
+                        while (m) {
+                            const int k = __ffs(m) - 1;
+                            m &= m - 1;
+                            hs += mix64(kz + __ldg(key + __ldg(p.g.col + rb + k)));
+                        }
+                    }
+                }
+            }
+        } else if (p.count) {
+            // phase D: closer rows in batches of kLeafBatch, all loads of a batch in flight
+            for (unsigned int q0 = 0; q0 < np; q0 += kLeafBatch) {
+                if (q0 > 0 && q0 % kLeafPairs == 0) {
+                    // (rare) more pairs than the list holds: rebuild the next window
+                    __syncwarp();
+                    unsigned int seen = 0;
+#pragma unroll
+                    for (int i = 0; i < kLeafPaths; ++i) {
+                        const bool anyext = __any_sync(FULL_MASK, ext[i] != 0ull);
+                        u64 zm = (anyext && mine) ? (above_word(v2v[i], lane) & ~(B[i] | a[i]) & a1[i]) : 0ull;
+                        const unsigned int pz = __popcll(zm);
+                        unsigned int incl = pz;
+#pragma unroll
+                        for (int d = 1; d < 32; d <<= 1) {
+                            const unsigned int t = __shfl_up_sync(FULL_MASK, incl, d);
+                            if (lane >= d)
+                                incl += t;
+                        }
+                        unsigned int pos = seen + incl - pz;
+                        while (zm) {
+                            const int b = __ffsll((long long)zm) - 1;
+                            zm &= zm - 1;
+                            if (pos >= q0 && pos < q0 + kLeafPairs)
+                                pair[pos - q0] = ((uint32_t)i << 12) | (uint32_t)(64 * lane + b);
+                            ++pos;
+                        }
+                        seen += __shfl_sync(FULL_MASK, incl, 31);
+                    }
+                    __syncwarp();
+                }
+                const uint32_t *pw = pair + (q0 % kLeafPairs);
+                u64 row[kLeafBatch];
+                uint32_t e[kLeafBatch];
+#pragma unroll
+                for (int k = 0; k < kLeafBatch; ++k) {
+                    e[k] = q0 + k < np ? pw[k] : 0xffffffffu;
+                    row[k] = (e[k] != 0xffffffffu && mine) ? __ldg(adj + (u64)(e[k] & 0xfffu) * NW + lane) : 0ull;
+                }
+#pragma unroll
+                for (int k = 0; k < kLeafBatch; ++k) {
+                    if (e[k] == 0xffffffffu)
+                        break;  // warp-uniform
+                    const uint32_t i = e[k] >> 12, z = e[k] & 0xfffu;
+                    u64 ex = ext[0], ks = KS[0];
+#pragma unroll
+                    for (int j = 1; j < kLeafPaths; ++j) {
+                        ex = i == (uint32_t)j ? ext[j] : ex;
+                        ks = i == (uint32_t)j ? KS[j] : ks;
+                    }
+                    u64 cl = row[k] & ex;
+                    if (cl) {
+                        lcyc += __popcll(cl);
+                        const u64 kz = ks + __ldg(key + z);
+                        while (cl) {
+                            const int b = __ffsll((long long)cl) - 1;
+                            cl &= cl - 1;
+                            hs += mix64(kz + __ldg(key + 64 * lane + b));
+                        }
+                    }
+                }
+            }
+        }
+        __syncwarp();
+    }
+    if (!p.count)
+        cand = 0;
     Acc acc;
     acc.cyc = cnt;
     acc.hash = hs;
     acc.cand = cand;
-    acc.cyc_next = leaf_cyc;
-    acc.cand_next = leaf_cand;
-    acc.paths_next = leaf_paths;
+    acc.cyc_next = lcyc;
+    acc.cand_next = lcand;
+    acc.paths_next = lpaths;
     flush(acc, p.sc);
 }
 
@@ -1492,6 +1647,21 @@ __global__ void __launch_bounds__(kBlock) k_shard_filter_wide(const LaunchArgs p
 }
 
 // ---------------------------------------------------------------------------- keys, collect
+// nbrmask[u*n + z] |= 1 << k for the k-th neighbour w of u and every z ~ w (one warp per u;
+// lane k < deg(u) <= 32 owns neighbour k)
+__global__ void k_build_nbrmask(const DevGraph g, uint32_t *T)
+{
+    const int u = blockIdx.x * (blockDim.x / 32) + (threadIdx.x >> 5), k = threadIdx.x & 31;
+    if (u >= g.n)
+        return;
+    const uint32_t b = g.rowptr[u], d = g.rowptr[u + 1] - b;
+    if ((uint32_t)k >= d)
+        return;
+    const uint32_t w = g.col[b + k];
+    for (uint32_t q = g.rowptr[w]; q < g.rowptr[w + 1]; ++q)
+        atomicOr(T + (u64)u * g.n + g.col[q], 1u << k);
+}
+
 __global__ void k_keys(u64 *key, const int32_t *orig, int n, u64 seed)
 {
     const int i = blockIdx.x * blockDim.x + threadIdx.x;
@@ -1657,7 +1827,7 @@ cudaError_t launch_wide(int which, const LaunchArgs &a, cudaStream_t st, int gri
     if (a.n_in == 0)
         return cudaSuccess;
     KernelFn f = which == 0 ? k_stage1_wide
-                 : which == 1 ? (a.emit && !a.emit_next ? k_expand_wide<true> : k_expand_wide<false>)
+                 : which == 1 ? (a.emit && !a.emit_next ? k_leaf_wide : k_expand_wide)
                               : k_shard_filter_wide;
     const u64 per_block = which == 1 ? (u64)(kBlock / 32) * kWidePaths : (u64)kBlock;
     return run(f, grid_for(per_block, a.n_in, grid_cap), 0, st, a);
@@ -1665,7 +1835,7 @@ cudaError_t launch_wide(int which, const LaunchArgs &a, cudaStream_t st, int gri
 
 int max_blocks_per_sm_wide(int which)
 {
-    KernelFn f = which == 0 ? k_stage1_wide : which == 1 ? k_expand_wide<false> : k_shard_filter_wide;
+    KernelFn f = which == 0 ? k_stage1_wide : which == 1 ? k_expand_wide : k_shard_filter_wide;
     int nb = 1;
     if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, (const void *)f, kBlock, 0) != cudaSuccess || nb < 1)
         nb = 1;
@@ -1716,6 +1886,14 @@ cudaError_t launch_keys(u64 *key, u64 *keybyte, const int32_t *orig, int n, int 
     k_keys<<<(n + 255) / 256, 256, 0, st>>>(key, orig, n, seed);
     if (nw <= kByteTableWords)
         k_keybyte<<<8 * nw, 256, 0, st>>>(keybyte, key, n);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_nbrmask(const DevGraph &g, uint32_t *T, cudaStream_t st)
+{
+    if (g.n <= 0)
+        return cudaSuccess;
+    k_build_nbrmask<<<(g.n + 7) / 8, 256, 0, st>>>(g, T);
     return cudaGetLastError();
 }
 
