@@ -83,3 +83,21 @@ def comb(a, b):
         return 0
     from math import comb as _c
     return _c(a, b)
+
+
+def hspec_hash_np(vertices, offsets, seed=DEFAULT_SEED):
+    """hspec_hash over many cycles at once (numpy, uint64 arithmetic wraps mod 2^64):
+    vertices int32[], offsets uint64[k+1] as returned by cc_fetch_cycles."""
+    import numpy as np
+
+    def mix(x):
+        x = x + np.uint64(0x9E3779B97F4A7C15)
+        x = (x ^ (x >> np.uint64(30))) * np.uint64(0xBF58476D1CE4E5B9)
+        x = (x ^ (x >> np.uint64(27))) * np.uint64(0x94D049BB133111EB)
+        return x ^ (x >> np.uint64(31))
+
+    with np.errstate(over="ignore"):
+        keys = mix(np.uint64(seed) ^ vertices.astype(np.uint64))
+        starts = offsets[:-1].astype(np.int64)
+        sums = np.add.reduceat(keys, starts) if len(starts) else np.zeros(0, np.uint64)
+        return int(mix(sums).sum(dtype=np.uint64))

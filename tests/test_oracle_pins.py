@@ -420,3 +420,16 @@ def test_csr_validation_error_kinds():
     col = np.array([1, 2, 1, 0, 2, 0, 1], dtype=np.int32)
     r = oracle.enumerate_cycles(3, rp, col)
     assert int(r["counts"][3]) == 1
+
+
+def test_hspec_hash_np_equals_scalar_definition():
+    """The vectorised host hash used by the collect-at-scale GPU test equals the scalar
+    H-spec definition (brute.hspec_hash) on random cycle lists."""
+    import numpy as np
+    from tests import brute
+    rng = np.random.default_rng(5)
+    sets = [list(rng.choice(1000, size=int(rng.integers(3, 12)), replace=False)) for _ in range(200)]
+    verts = np.array([v for s in sets for v in s], dtype=np.int32)
+    offs = np.zeros(len(sets) + 1, dtype=np.uint64)
+    offs[1:] = np.cumsum([len(s) for s in sets])
+    assert brute.hspec_hash_np(verts, offs) == brute.hspec_hash([[int(v) for v in s] for s in sets])
