@@ -74,6 +74,10 @@ def _load():
             ctypes.c_uint64, ctypes.c_uint64, P, P, P, P, P, ctypes.c_uint64, P,
             ctypes.c_uint64, P,
         ]
+        lib.orc_enumerate_split.restype = ctypes.c_int
+        lib.orc_enumerate_split.argtypes = [
+            ctypes.c_int64, P, P, ctypes.c_uint32, ctypes.c_uint64, ctypes.c_int, ctypes.c_int, P, P, P, P,
+        ]
         _lib = lib
     return _lib
 
@@ -161,3 +165,20 @@ def enumerate_cycles(n, row_ptr, col, max_len: int = 0, seed: int = DEFAULT_SEED
         k = int(ncyc[0])
         out["cycles"] = [verts[int(offs[i]):int(offs[i + 1])].tolist() for i in range(k)]
     return out
+
+
+def enumerate_cycles_split(n, row_ptr, col, max_len: int = 0, seed: int = DEFAULT_SEED,
+                           nthreads: int = 1, split_len: int = 16):
+    """Count mode of enumerate_cycles with a balanced multi-thread schedule for large runs
+    (orc_enumerate_split): Alg. 1 down to paths of split_len vertices on one thread, then the
+    subtrees of those paths on nthreads threads.  Same outputs as enumerate_cycles."""
+    n, row_ptr, col = _csr(n, row_ptr, col)
+    counts = np.zeros(n + 1, dtype=np.uint64)
+    pbl = np.zeros(n + 1, dtype=np.uint64)
+    h = np.zeros(1, dtype=np.uint64)
+    cand = np.zeros(1, dtype=np.uint64)
+    rc = _load().orc_enumerate_split(n, _ptr(row_ptr), _ptr(col), max_len, seed, nthreads, split_len,
+                                     _ptr(counts), _ptr(h), _ptr(pbl), _ptr(cand))
+    if rc != 0:
+        raise OracleError(rc)
+    return dict(counts=counts, set_hash=int(h[0]), paths_by_len=pbl, candidates=int(cand[0]))

@@ -272,6 +272,10 @@ typedef struct {
     uint64_t *paths_by_len; /* [n+2] paths scanned by the expansion, by vertex count */
     uint64_t candidates;    /* sum over scanned paths of deg(v_t) */
     int32_t *path;          /* current path <v1..vt> */
+    /* orc_enumerate_split only: paths of split_len vertices are queued, not visited */
+    int split_len;
+    int32_t *items;
+    int64_t n_items, items_cap;
     /* optional cycle list */
     int32_t *cyc_vertices;
     uint64_t cyc_vertices_cap;
@@ -313,6 +317,17 @@ static void og_record(og_ctx *cx, const int32_t *c, int k)
  * for each v in Adj(vt): if l(v) > l(v2) and v is not adjacent to v_i, i in {2..t-1}
  * (and v not in p, Alg. 3 line 11 / reading G6), then either v in Adj(v1) -> cycle
  * <p,v>, or <p,v> is a new chordless path that is visited recursively (DFS). */
+/* orc_enumerate_split: append the current path of t vertices to the work queue */
+static void og_queue(og_ctx *cx, int t)
+{
+    if (cx->n_items == cx->items_cap) {
+        cx->items_cap = cx->items_cap ? 2 * cx->items_cap : 1024;
+        cx->items = (int32_t *)realloc(cx->items, (size_t)cx->items_cap * (size_t)t * sizeof(int32_t));
+    }
+    memcpy(cx->items + cx->n_items * t, cx->path, (size_t)t * sizeof(int32_t));
+    cx->n_items++;
+}
+
 static void og_visit(og_ctx *cx, int t)
 {
     const og_graph *g = cx->g;
@@ -343,7 +358,10 @@ static void og_visit(og_ctx *cx, int t)
         if (g->adj[(int64_t)v * n + v1]) {
             og_record(cx, p, t + 1);
         } else if (cx->max_len == 0 || (uint32_t)(t + 1) < cx->max_len) {
-            og_visit(cx, t + 1);
+            if (cx->split_len > 0 && t + 1 == cx->split_len)
+                og_queue(cx, t + 1);  /* visited later by a worker thread */
+            else
+                og_visit(cx, t + 1);
         }
     }
 }
@@ -498,4 +516,114 @@ int orc_validate(int64_t n, const int64_t *row_ptr, const int32_t *col)
     if (rc == ORC_OK)
         og_free(&g);
     return rc;
+}
+
+/* ---------------------------------------------------------------- parallel driver (large runs)
+ * The same visits as orc_enumerate, scheduled for many threads when there are few triplets
+ * (a grid has ~n of them, with very unequal subtrees): Alg. 1 runs on one thread down to the
+ * paths of split_len vertices, which are queued instead of visited; nthreads workers then take
+ * queued paths one at a time (shared counter) and finish each with the same og_visit.  Every
+ * path is visited exactly once and every sum is order-independent, so the outputs equal
+ * orc_enumerate's (pinned by tests/test_oracle_pins.py).  Count mode only.  */
+typedef struct {
+    og_ctx cx;
+    og_ctx *root;
+    int64_t *next;
+} og_split_worker;
+
+static void *og_split_main(void *arg)
+{
+    og_split_worker *w = (og_split_worker *)arg;
+    const og_ctx *r = w->root;
+    const int L = r->split_len;
+    for (;;) {
+        int64_t i = __atomic_fetch_add(w->next, 1, __ATOMIC_RELAXED);
+        if (i >= r->n_items)
+            break;
+        memcpy(w->cx.path, r->items + i * L, (size_t)L * sizeof(int32_t));
+        og_visit(&w->cx, L);
+    }
+    return NULL;
+}
+
+int orc_enumerate_split(int64_t n, const int64_t *row_ptr, const int32_t *col, uint32_t max_len,
+                        uint64_t seed, int nthreads, int split_len, uint64_t *counts, uint64_t *set_hash,
+                        uint64_t *paths_by_len, uint64_t *candidates)
+{
+    if (seed == 0)
+        seed = 0x1410487600000000ULL;
+    if (nthreads < 1 || split_len < 4)
+        return ORC_ERR_INVALID_ARGUMENT;
+    og_graph g;
+    int rc = og_setup(&g, n, row_ptr, col, NULL, seed);
+    if (rc != ORC_OK)
+        return rc;
+    int64_t ntri = 0;
+    int64_t nt = og_triplets(&g, NULL, 0, NULL, 0, &ntri);
+    og_triplet *trip = (og_triplet *)malloc((size_t)(nt > 0 ? nt : 1) * sizeof(og_triplet));
+    og_triplet *tri = (og_triplet *)malloc((size_t)(ntri > 0 ? ntri : 1) * sizeof(og_triplet));
+    og_triplets(&g, trip, nt, tri, ntri, &ntri);
+    og_split_worker *ws = (og_split_worker *)calloc((size_t)nthreads + 1, sizeof(og_split_worker));
+    for (int i = 0; i <= nthreads; i++) {
+        og_ctx *cx = &ws[i].cx;
+        cx->g = &g;
+        cx->max_len = max_len;
+        cx->counts = (uint64_t *)calloc((size_t)n + 2, sizeof(uint64_t));
+        cx->paths_by_len = (uint64_t *)calloc((size_t)n + 2, sizeof(uint64_t));
+        cx->path = (int32_t *)calloc((size_t)n + 2, sizeof(int32_t));
+    }
+    og_ctx *root = &ws[nthreads].cx; /* the single-threaded prefix phase */
+    root->split_len = split_len;
+    if (max_len == 0 || max_len >= 3) {
+        for (int64_t i = 0; i < ntri; i++) {
+            int32_t c[3] = {tri[i].x, tri[i].u, tri[i].y};
+            og_record(root, c, 3);
+        }
+    }
+    if (max_len == 0 || max_len >= 4) {
+        for (int64_t i = 0; i < nt; i++) {
+            root->path[0] = trip[i].x;
+            root->path[1] = trip[i].u;
+            root->path[2] = trip[i].y;
+            og_visit(root, 3);
+        }
+    }
+    int64_t next = 0;
+    pthread_t *th = (pthread_t *)calloc((size_t)nthreads, sizeof(pthread_t));
+    for (int i = 0; i < nthreads; i++) {
+        ws[i].root = root;
+        ws[i].next = &next;
+        pthread_create(&th[i], NULL, og_split_main, &ws[i]);
+    }
+    for (int i = 0; i < nthreads; i++)
+        pthread_join(th[i], NULL);
+    free(th);
+    for (int64_t k = 0; k <= n; k++) {
+        counts[k] = 0;
+        if (paths_by_len)
+            paths_by_len[k] = 0;
+    }
+    *set_hash = 0;
+    if (candidates)
+        *candidates = 0;
+    for (int i = 0; i <= nthreads; i++) {
+        og_ctx *cx = &ws[i].cx;
+        for (int64_t k = 0; k <= n; k++) {
+            counts[k] += cx->counts[k];
+            if (paths_by_len)
+                paths_by_len[k] += cx->paths_by_len[k];
+        }
+        *set_hash += cx->set_hash;
+        if (candidates)
+            *candidates += cx->candidates;
+        free(cx->counts);
+        free(cx->paths_by_len);
+        free(cx->path);
+        free(cx->items);
+    }
+    free(ws);
+    free(trip);
+    free(tri);
+    og_free(&g);
+    return ORC_OK;
 }

@@ -20,11 +20,14 @@ import oracle  # noqa: E402
 from paper_1410_4876_b200 import inputs  # noqa: E402
 
 CONFIGS = {
-    "p10x10": dict(graph=lambda: inputs.grid(10, 10), max_len=0),
-    "grid8x10": dict(graph=lambda: inputs.grid(8, 10), max_len=0),
-    "grid9x9": dict(graph=lambda: inputs.grid(9, 9), max_len=0),
+    "p10x10": dict(graph=lambda: inputs.grid(10, 10), max_len=0, split_len=18),
+    "grid8x10": dict(graph=lambda: inputs.grid(8, 10), max_len=0, split_len=16),
+    "grid9x9": dict(graph=lambda: inputs.grid(9, 9), max_len=0, split_len=16),
     "gnp2000_k8": dict(graph=lambda: inputs.gnp(2000, 0.005, inputs.GNP_SEED), max_len=8),
     "gnp2000_k9": dict(graph=lambda: inputs.gnp(2000, 0.005, inputs.GNP_SEED), max_len=9),
+    "gnp2000_k10": dict(graph=lambda: inputs.gnp(2000, 0.005, inputs.GNP_SEED), max_len=10),
+    "k150": dict(graph=lambda: inputs.complete_bipartite(150, 150), max_len=0),
+    "p8x8": dict(graph=lambda: inputs.grid(8, 8), max_len=0, split_len=12),
 }
 
 
@@ -36,7 +39,10 @@ def main():
     cfg = CONFIGS[a.name]
     g = cfg["graph"]()
     t0 = time.time()
-    r = oracle.enumerate_cycles(*g, max_len=cfg["max_len"], nthreads=a.threads)
+    # balanced schedule (orc_enumerate_split, pinned equal to orc_enumerate by
+    # tests/test_oracle_pins.py::test_split_driver_equals_sequential_oracle)
+    r = oracle.enumerate_cycles_split(*g, max_len=cfg["max_len"], nthreads=a.threads,
+                                      split_len=cfg.get("split_len", 8))
     dt = time.time() - t0
     out = {
         "name": a.name, "n": g[0], "m": len(g[2]) // 2, "max_len": cfg["max_len"],
@@ -44,7 +50,7 @@ def main():
         "total": int(r["counts"].sum()), "set_hash": f"{r['set_hash']:#018x}",
         "paths_by_len": {str(k): int(v) for k, v in enumerate(r["paths_by_len"]) if v},
         "paths_total": int(r["paths_by_len"].sum()), "candidates": r["candidates"],
-        "oracle_seconds": dt, "oracle_threads": a.threads,
+        "oracle_seconds": dt, "oracle_threads": a.threads, "split_len": cfg.get("split_len", 8),
         "generated_by": "tests/golden/make_oracle_big.py (oracle/ only)",
     }
     with open(os.path.join(HERE, f"oracle_{a.name}.json"), "w") as f:

@@ -373,3 +373,35 @@ def test_k150_collect_at_scale(ws):
     codes = np.concatenate(codes)
     assert len(np.unique(codes)) == total
     assert hs == h
+
+
+GOLDEN = os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden")
+BIG = {
+    "p8x8": (lambda: I.grid(8, 8), 0), "k150": (lambda: I.complete_bipartite(150, 150), 0),
+    "grid8x10": (lambda: I.grid(8, 10), 0), "gnp2000_k9": (lambda: I.gnp(2000, 0.005, I.GNP_SEED), 9),
+    "gnp2000_k10": (lambda: I.gnp(2000, 0.005, I.GNP_SEED), 10), "p10x10": (lambda: I.grid(10, 10), 0),
+}
+
+
+@pytest.mark.parametrize("name", sorted(BIG))
+def test_full_size_against_oracle_golden(ws, name):
+    """The BASELINE configs at full size, in the launch configuration bench.py times (a large
+    arena, count mode): counts, set hash, |F_t| and candidates equal the oracle's, stored in
+    tests/golden/oracle_<name>.json by tests/golden/make_oracle_big.py (oracle/ only)."""
+    import json
+
+    import torch
+    path = os.path.join(GOLDEN, f"oracle_{name}.json")
+    if not os.path.exists(path):
+        pytest.skip(f"{path} not generated yet")
+    want = json.load(open(path))
+    build_g, K = BIG[name]
+    assert want["max_len"] == K
+    free, _ = torch.cuda.mem_get_info()
+    big = torch.empty(int(free * 0.8), dtype=torch.uint8, device="cuda")
+    got = binding.enumerate_cycles(*build_g(), workspace=big, max_len=K)
+    del big
+    assert {str(k): int(v) for k, v in enumerate(got["counts"]) if v} == want["counts"]
+    assert f"{got['set_hash']:#018x}" == want["set_hash"]
+    assert {str(k): int(v) for k, v in enumerate(got["paths_by_len"]) if v} == want["paths_by_len"]
+    assert got["candidates"] == want["candidates"]

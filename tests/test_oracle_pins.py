@@ -433,3 +433,19 @@ def test_hspec_hash_np_equals_scalar_definition():
     offs = np.zeros(len(sets) + 1, dtype=np.uint64)
     offs[1:] = np.cumsum([len(s) for s in sets])
     assert brute.hspec_hash_np(verts, offs) == brute.hspec_hash([[int(v) for v in s] for s in sets])
+
+
+@pytest.mark.parametrize("name,g,K,L", [
+    ("grid6x7", I.grid(6, 7), 0, 9), ("grid5x6", I.grid(5, 6), 0, 4), ("k8x8", I.complete_bipartite(8, 8), 0, 4),
+    ("wheel12", I.wheel(12), 0, 6), ("gnp80", I.gnp(80, 0.1, 77), 8, 6), ("gnp80_deep_split", I.gnp(80, 0.1, 77), 8, 30),
+])
+def test_split_driver_equals_sequential_oracle(name, g, K, L):
+    """orc_enumerate_split (the balanced multi-thread schedule used for the large golden files)
+    gives exactly orc_enumerate's counts, hash, |F_t| and candidates, for split depths inside,
+    at and beyond the deepest level."""
+    a = oracle.enumerate_cycles(*g, max_len=K)
+    b = oracle.enumerate_cycles_split(*g, max_len=K, nthreads=4, split_len=L)
+    assert a["counts"].tolist() == b["counts"].tolist()
+    assert a["set_hash"] == b["set_hash"]
+    assert a["paths_by_len"].tolist() == b["paths_by_len"].tolist()
+    assert a["candidates"] == b["candidates"]
