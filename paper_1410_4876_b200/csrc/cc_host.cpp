@@ -17,6 +17,7 @@
 #include "cc_internal.h"
 
 #include <algorithm>
+#include <functional>
 #include <chrono>
 #include <cmath>
 #include <cstddef>
@@ -121,29 +122,36 @@ extern "C" const char *cc_status_string(cc_status s)
 extern "C" const char *cc_version(void) { return "chordless-b200 0.1 (sm_100a)"; }
 
 // Degree labelling: repeatedly delete a vertex of minimum degree in the
-// remaining graph, l(u_i) = i; ties to the lowest original id.  Ordered set keyed
-// (degree, id), O((n + m) log n).
+// remaining graph, l(u_i) = i; ties to the lowest original id.  Binary min-heap keyed
+// (degree, id) with lazy deletion (a decremented vertex is pushed again; stale entries are
+// skipped when popped): O((n + m) log(n + m)) with vector-backed constants.
 static void degree_labeling(int64_t n, const std::vector<int64_t> &rp, const std::vector<int32_t> &cl,
                             std::vector<int32_t> &label)
 {
+    typedef std::pair<int64_t, int32_t> Key;
     std::vector<int64_t> d(n);
-    std::set<std::pair<int64_t, int32_t>> q;
+    std::vector<Key> heap;
+    heap.reserve((size_t)n + cl.size());
     for (int64_t v = 0; v < n; ++v) {
         d[v] = rp[v + 1] - rp[v];
-        q.insert({d[v], (int32_t)v});
+        heap.push_back({d[v], (int32_t)v});
     }
+    std::make_heap(heap.begin(), heap.end(), std::greater<Key>());
     label.assign(n, -1);
-    for (int64_t i = 0; i < n; ++i) {
-        auto it = q.begin();
-        const int32_t u = it->second;
-        q.erase(it);
-        label[u] = (int32_t)i;
+    for (int64_t i = 0; i < n;) {
+        std::pop_heap(heap.begin(), heap.end(), std::greater<Key>());
+        const Key top = heap.back();
+        heap.pop_back();
+        const int32_t u = top.second;
+        if (label[u] >= 0 || top.first != d[u])
+            continue;  // stale entry
+        label[u] = (int32_t)i++;
         for (int64_t k = rp[u]; k < rp[u + 1]; ++k) {
             const int32_t w = cl[k];
             if (label[w] < 0) {
-                q.erase({d[w], w});
                 --d[w];
-                q.insert({d[w], w});
+                heap.push_back({d[w], w});
+                std::push_heap(heap.begin(), heap.end(), std::greater<Key>());
             }
         }
     }
