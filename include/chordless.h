@@ -88,6 +88,11 @@ typedef struct {
                                  of the graph, shard_count and min_shard_paths -- and, only when an
                                  unsharded level does not fit the arena, of the arena size: give
                                  every rank the same workspace_bytes */
+    uint32_t record_format;   /* frontier record format: 0 = automatic, 1 = blocked
+                                 set (every size class), 2 = vertex list (count mode, 512 < n <=
+                                 2015, max degree <= 32, 4 <= max_len <= 14; otherwise
+                                 CC_ERR_INVALID_ARGUMENT).  Automatic picks the list for the
+                                 graphs it accepts.  Results do not depend on it. */
 } cc_options;
 
 /* Statistics of one cc_enumerate call (cc_result_stats). */

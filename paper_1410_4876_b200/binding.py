@@ -45,7 +45,7 @@ class cc_options(ctypes.Structure):
         ("root_offset", ctypes.c_uint64), ("hash_seed", ctypes.c_uint64),
         ("workspace", ctypes.c_void_p), ("workspace_bytes", ctypes.c_uint64),
         ("collect_capacity", ctypes.c_uint64), ("profile", ctypes.c_uint32),
-        ("min_shard_paths", ctypes.c_uint32),
+        ("min_shard_paths", ctypes.c_uint32), ("record_format", ctypes.c_uint32),
     ]
 
 
@@ -183,7 +183,8 @@ def cc_graph_labels(g: Graph) -> np.ndarray:
 def make_options(device: int = -1, stream=None, max_len: int = 0, collect: bool = False,
                  shard_index: int = 0, shard_count: int = 1, root_stride: int = 0,
                  root_offset: int = 0, hash_seed: int = 0, workspace=None, workspace_bytes: int = 0,
-                 collect_capacity: int = 0, profile: bool = False, min_shard_paths: int = 0):
+                 collect_capacity: int = 0, profile: bool = False, min_shard_paths: int = 0,
+                 record_format: int = 0):
     o = cc_options()
     load().cc_options_init(ctypes.byref(o))
     o.device = device
@@ -207,6 +208,7 @@ def make_options(device: int = -1, stream=None, max_len: int = 0, collect: bool 
     o.collect_capacity = collect_capacity
     o.profile = 1 if profile else 0
     o.min_shard_paths = min_shard_paths
+    o.record_format = record_format
     return o
 
 

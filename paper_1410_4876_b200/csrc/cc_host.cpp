@@ -532,7 +532,19 @@ static cc_status enumerate_impl(const cc_graph *cg, const cc_options *opt_in, cc
     // B-mode records carry v1, v2, vt in the spare top bits of the blocked set when n allows
     const bool wide = g->wide;
     const bool packed = wide || (mode == cc::Mode::B && cc::packable(nw, (int)n));
-    const u64 rec_bytes = (u64)cc::record_bytes(nw, mode, packed);
+    // list class: the path's vertex list instead of its blocked set, for sparse
+    // wide graphs under a length cap (written paths have <= max(3, max_len - 2) vertices)
+    const bool list_ok = wide && mode == cc::Mode::B && opt.max_len >= 4 && opt.max_len <= (uint32_t)cc::kListMaxLen &&
+                         g->max_deg <= 32;
+    if (opt.record_format > 2)
+        return fail(CC_ERR_INVALID_ARGUMENT, "record_format must be 0, 1 or 2");
+    if (opt.record_format == 2 && !list_ok)
+        return fail(CC_ERR_INVALID_ARGUMENT, "record_format 2 (vertex list) needs count mode, 512 < n <= 2015, "
+                                             "max degree <= 32 and 4 <= max_len <= " +
+                                                 std::to_string(cc::kListMaxLen));
+    const bool list = opt.record_format == 2 || (opt.record_format == 0 && list_ok);
+    const int rwl = list ? std::max<int>(2, (std::max<int>(3, (int)opt.max_len - 2) + 3) / 4) : 0;
+    const u64 rec_bytes = list ? (u64)(rwl + 1) * 8 : (u64)cc::record_bytes(nw, mode, packed);
     S.record_bytes = rec_bytes;
 
     // ---- frontier arena, split into pages of P = 2^lp records
@@ -614,12 +626,15 @@ static cc_status enumerate_impl(const cc_graph *cg, const cc_options *opt_in, cc
                                       : g->max_deg <= 32                      ? cc::ExpandVariant::Thread
                                                                               : cc::ExpandVariant::Warp;
     const size_t gsmem = ((size_t)n * (nw + 1) + (nw <= cc::kByteTableWords ? (size_t)8 * nw * 256 : 0)) * 8;
-    const int grid_s1 = (wide ? cc::max_blocks_per_sm_wide(0) : cc::max_blocks_per_sm(0, mode, nw, packed, gsmem)) * sms;
+    const int grid_s1 = (list ? cc::max_blocks_per_sm_list(0, rwl)
+                         : wide ? cc::max_blocks_per_sm_wide(0) : cc::max_blocks_per_sm(0, mode, nw, packed, gsmem)) * sms;
     const int grid_ex =
-        (wide ? cc::max_blocks_per_sm_wide(1)
+        (list ? cc::max_blocks_per_sm_list(1, rwl)
+         : wide ? cc::max_blocks_per_sm_wide(1)
               : cc::max_blocks_per_sm(variant == cc::ExpandVariant::Small ? 4 : variant == cc::ExpandVariant::Thread ? 1 : 2,
                                       mode, nw, packed, cc::expand_smem(mode, nw, (int)n, packed))) * sms;
-    const int grid_sf = (wide ? cc::max_blocks_per_sm_wide(2) : cc::max_blocks_per_sm(3, mode, nw, packed, 0)) * sms;
+    const int grid_sf = (list ? cc::max_blocks_per_sm_list(2, rwl)
+                         : wide ? cc::max_blocks_per_sm_wide(2) : cc::max_blocks_per_sm(3, mode, nw, packed, 0)) * sms;
     const double maxfan = (double)std::max<int64_t>(g->max_deg - 1, 1);
     const uint32_t W = opt.shard_count;
     // Multi-GPU partition: the first frontier level with >= threshold paths is
@@ -701,7 +716,11 @@ static cc_status enumerate_impl(const cc_graph *cg, const cc_options *opt_in, cc
         a.filter = filter ? 1 : 0;
         if (opt.profile)
             CC_CUDA(cudaEventRecord(ea, st));
-        if (wide)
+        a.tlen = (uint32_t)trace_level;  // vertices per input path of an expansion
+        if (list)
+            CC_CUDA(cc::launch_list(kind == STAGE1 ? 0 : kind == EXPAND ? 1 : 2, a, rwl, leaf, st,
+                                    kind == STAGE1 ? grid_s1 : kind == EXPAND ? grid_ex : grid_sf));
+        else if (wide)
             CC_CUDA(cc::launch_wide(kind == STAGE1 ? 0 : kind == EXPAND ? 1 : 2, a, st,
                                     kind == STAGE1 ? grid_s1 : kind == EXPAND ? grid_ex : grid_sf));
         else if (kind == STAGE1)

@@ -107,6 +107,7 @@ struct LaunchArgs {
     uint32_t shard_count;
     uint32_t idb;                // packed records: bits per id (ids in the top 3*idb bits of word NW-1)
     uint32_t packed;             // 1 = B-mode record with packed ids (no ids array)
+    uint32_t tlen;               // list records: vertices per input path (Stage 2)
 };
 
 // Thread: thread per path; Warp: warp per path (S-mode, Delta > 32); Small: B-mode with
@@ -147,6 +148,12 @@ size_t expand_smem(Mode m, int nw, int n, bool packed);
 cudaError_t launch_wide(int which, const LaunchArgs &a, cudaStream_t st, int grid_cap);
 int max_blocks_per_sm_wide(int which);
 constexpr int kWideMaxWords = 32;
+// List class (count mode, wide graphs with Delta <= 32): a path is its vertex list, 16-bit ids,
+// four per word (RWL id words), plus keysum(p); SoA pages like every other record.
+// which: 0 = Stage 1, 1 = expand (leaf = last-level fusion), 2 = shard filter.
+cudaError_t launch_list(int which, const LaunchArgs &a, int rwl, bool leaf, cudaStream_t st, int grid_cap);
+int max_blocks_per_sm_list(int which, int rwl);
+constexpr int kListMaxLen = 14;  // max_len <= 14: written paths have <= 12 vertices (3 id words)
 // Resident CTAs per SM at kBlock threads with the given dynamic smem.
 // which: 0 = Stage 1, 1 = expand (thread), 2 = expand (warp), 3 = shard filter, 4 = expand (small)
 int max_blocks_per_sm(int which, Mode m, int nw, bool packed, size_t smem);

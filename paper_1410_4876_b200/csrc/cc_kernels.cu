@@ -1646,6 +1646,240 @@ __global__ void __launch_bounds__(kBlock) k_shard_filter_wide(const LaunchArgs p
     }
 }
 
+// ---------------------------------------------------------------------------- list class
+// Sparse wide graphs (count mode, 512 < n <= 2015, Delta <= 32, max_len <= 14).  A path is its
+// vertex list v1..vt (16-bit ids, four per word) plus keysum(p): 24 B for t <= 8 instead of a
+// 2000-bit blocked set.  One thread per path.  With the neighbour-mask table T = nbrmask
+// (bit k of T[u][z] = "k-th neighbour of u is adjacent to z"), the test of Alg. 3 lines 11-14
+// becomes 32-bit masks over the CSR row of vt (positions k, candidate v_k = col[row(vt) + k]):
+//   blocked = OR over the interior vertices x = v2..v_{t-1} of T[vt][x]   (v in B(p))
+//   Cand    = valid & {k : v_k > v2} & ~blocked
+//   Close   = Cand & T[vt][v1],   Ext = Cand & ~T[vt][v1]
+// (open rows suffice: the only path vertex in Adj(vt) is v_{t-1}, which is adjacent to the
+// interior v_{t-2}, or is v2 itself when t = 3 and fails the gate).  Last-level fusion: the
+// closers of the children lie in the row of v1, Z = {k : w_k > v2} & ~OR_{x in v2..vt} T[v1][x],
+// and child v closes through the positions T[v1][v] & Z.
+__device__ __forceinline__ uint32_t list_id(const u64 *W, int i)
+{
+    return (uint32_t)(W[i >> 2] >> (16 * (i & 3))) & 0xffffu;
+}
+
+// number of entries <= x in the sorted row col[b .. b+d)
+__device__ __forceinline__ uint32_t row_rank(const uint32_t *col, uint32_t b, uint32_t d, uint32_t x)
+{
+    uint32_t lo = 0, hi = d;
+    while (lo < hi) {
+        const uint32_t mid = (lo + hi) >> 1;
+        if (__ldg(col + b + mid) <= x)
+            lo = mid + 1;
+        else
+            hi = mid;
+    }
+    return lo;
+}
+
+__device__ __forceinline__ uint32_t low_mask(uint32_t k)  // bits 0..k-1 (k <= 32)
+{
+    return k >= 32 ? 0xffffffffu : ((1u << k) - 1u);
+}
+
+template <int RWL>
+__global__ void __launch_bounds__(kBlock) k_stage1_list(const LaunchArgs p)
+{
+    constexpr int RW = RWL + 1;
+    __shared__ ReserveSmem rs;
+    const int n = p.g.n, NW = p.g.nw;
+    const u64 *__restrict__ adj = p.g.adj;
+    const u64 *__restrict__ key = p.g.key;
+    u64 cnt = 0, hs = 0;
+    const u64 stride = (u64)gridDim.x * kBlock;
+    for (u64 base = (u64)blockIdx.x * kBlock; base < p.n_in; base += stride) {
+        const u64 r = base + threadIdx.x;
+        unsigned int emit = 0;
+        u64 W[RW];
+#pragma unroll
+        for (int w = 0; w < RW; ++w)
+            W[w] = 0;
+        if (r < p.n_in) {
+            const u64 gid = p.in_lo + r;
+            int lo = 0, hi = n - 1;
+            while (lo < hi) {
+                const int mid = (lo + hi + 1) >> 1;
+                if (p.g.pair_prefix[mid] <= gid)
+                    lo = mid;
+                else
+                    hi = mid - 1;
+            }
+            const uint32_t u = (uint32_t)lo;
+            const u64 q = gid - p.g.pair_prefix[u];
+            u64 j = (u64)((1.0 + sqrt(1.0 + 8.0 * (double)q)) * 0.5);
+            while (j * (j - 1) / 2 > q)
+                --j;
+            while ((j + 1) * j / 2 <= q)
+                ++j;
+            const u64 i = q - j * (j - 1) / 2;
+            const uint32_t f = p.g.fwd[u];
+            const uint32_t x = p.g.col[f + (uint32_t)i];
+            const uint32_t y = p.g.col[f + (uint32_t)j];  // u < x < y (Alg. 2 l.12)
+            const bool tri = (__ldg(adj + (u64)x * NW + (y >> 6)) >> (y & 63)) & 1ull;
+            if (tri) {
+                if (p.count) {
+                    cnt++;
+                    hs += mix64(__ldg(key + x) + __ldg(key + u) + __ldg(key + y));
+                }
+            } else if (p.emit) {
+                emit = 1;
+                if (p.root_stride > 1) {
+                    const u64 rkey = ((u64)p.g.orig[x] << 42) | ((u64)p.g.orig[u] << 21) | (u64)p.g.orig[y];
+                    emit = (mix64(rkey) % p.root_stride) == p.root_offset;
+                }
+                W[0] = (u64)x | ((u64)u << 16) | ((u64)y << 32);  // <x, u, y>
+                W[RWL] = __ldg(key + x) + __ldg(key + u) + __ldg(key + y);
+                if (emit && p.filter)
+                    emit = (shard_hash<RW>(W, 0) % p.shard_count) == p.shard_index;
+            }
+        }
+        const u64 off = block_reserve(emit, &p.sc->out_count, rs);
+        if (emit) {
+            if (off >= p.out_cap)
+                p.sc->err = 1;
+            else
+                store_record<RW, false>(p.pg, p.out_off + off, W, 0);
+        }
+    }
+    flush_accum(cnt, hs, 0, p.sc);
+}
+
+template <int RWL, bool LEAF>
+__global__ void __launch_bounds__(kBlock) k_expand_list(const LaunchArgs p)
+{
+    constexpr int RW = RWL + 1;
+    __shared__ ReserveSmem rs;
+    __shared__ uint16_t s_deg[2048];
+    const int t = (int)p.tlen;
+    const uint32_t n = (uint32_t)p.g.n;
+    const uint32_t *__restrict__ T = p.g.nbrmask;
+    const uint32_t *__restrict__ col = p.g.col;
+    const uint32_t *__restrict__ rowptr = p.g.rowptr;
+    const u64 *__restrict__ key = p.g.key;
+    for (uint32_t v = threadIdx.x; v < n; v += kBlock)
+        s_deg[v] = (uint16_t)(rowptr[v + 1] - rowptr[v]);
+    __syncthreads();
+    const u64 pmask = (1ull << p.pg.log_p) - 1;
+    u64 cnt = 0, hs = 0, cand = 0, lpaths = 0, lcand = 0, lcyc = 0;
+    const u64 stride = (u64)gridDim.x * kBlock;
+    for (u64 base = (u64)blockIdx.x * kBlock; base < p.n_in; base += stride) {
+        const u64 r = base + threadIdx.x;
+        u64 W[RW];
+        uint32_t ext = 0, rb = 0;
+        if (r < p.n_in) {
+            const char *pp = page_ptr(p.pg, p.pg.in_pages[r >> p.pg.log_p]);
+            const u64 slot = r & pmask;
+#pragma unroll
+            for (int w = 0; w < RW; ++w)
+                W[w] = ((const u64 *)pp)[((u64)w << p.pg.log_p) + slot];
+            // (positions unrolled so that W stays in registers)
+            const uint32_t v1 = list_id(W, 0), v2 = list_id(W, 1);
+            uint32_t vt;
+            {
+                const int q = t - 1;  // word q / 4, lane q % 4 (scalar selects: no local memory)
+                const u64 wq = q < 4 ? W[0] : (q < 8 || RWL < 3 ? W[1] : W[RWL - 1]);
+                vt = (uint32_t)(wq >> (16 * (q & 3))) & 0xffffu;
+            }
+            const u64 ks = W[RWL];
+            rb = __ldg(rowptr + vt);
+            const uint32_t dt = s_deg[vt];
+            const u64 trow = (u64)vt * n;
+            uint32_t blocked = 0;
+#pragma unroll
+            for (int q = 1; q < 4 * RWL; ++q)
+                if (q < t - 1)
+                    blocked |= __ldg(T + trow + list_id(W, q));
+            const uint32_t a1m = __ldg(T + trow + v1);
+            const uint32_t cm = low_mask(dt) & ~low_mask(row_rank(col, rb, dt, v2)) & ~blocked;
+            uint32_t close = cm & a1m;
+            ext = p.emit ? (cm & ~a1m) : 0u;
+            if (p.count) {
+                cand += dt;
+                cnt += __popc(close);
+                while (close) {
+                    const int k = __ffs(close) - 1;
+                    close &= close - 1;
+                    hs += mix64(ks + __ldg(key + __ldg(col + rb + k)));
+                }
+            }
+            if (LEAF) {
+                if (ext && p.count) {
+                    const uint32_t rb1 = __ldg(rowptr + v1), d1 = s_deg[v1];
+                    const u64 t1 = (u64)v1 * n;
+                    uint32_t blk1 = 0;
+#pragma unroll
+                    for (int q = 1; q < 4 * RWL; ++q)  // v2 .. vt
+                        if (q < t)
+                            blk1 |= __ldg(T + t1 + list_id(W, q));
+                    const uint32_t Z = low_mask(d1) & ~low_mask(row_rank(col, rb1, d1, v2)) & ~blk1;
+                    uint32_t m = ext;
+                    while (m) {
+                        const int k = __ffs(m) - 1;
+                        m &= m - 1;
+                        const uint32_t v = __ldg(col + rb + k);
+                        lpaths++;
+                        lcand += s_deg[v];
+                        uint32_t c2 = Z ? (__ldg(T + t1 + v) & Z) : 0u;
+                        if (c2) {
+                            lcyc += __popc(c2);
+                            const u64 kv = ks + __ldg(key + v);
+                            while (c2) {
+                                const int j = __ffs(c2) - 1;
+                                c2 &= c2 - 1;
+                                hs += mix64(kv + __ldg(key + __ldg(col + rb1 + j)));
+                            }
+                        }
+                    }
+                }
+                ext = 0;
+            }
+        }
+        const unsigned int ne = __popc(ext);
+        const u64 off = block_reserve(ne, &p.sc->out_count, rs);
+        if (ne) {
+            if (off + ne > p.out_cap) {
+                p.sc->err = 1;
+            } else {
+                // children <p, v>: the parent's list with v appended, keysum + key(v)
+                const int wv = t >> 2, sh = 16 * (t & 3);
+                u64 o = p.out_off + off;
+                uint32_t m = ext;
+                while (m) {
+                    const int k = __ffs(m) - 1;
+                    m &= m - 1;
+                    const uint32_t v = __ldg(col + rb + k);
+                    u64 C[RW];
+#pragma unroll
+                    for (int w = 0; w < RW; ++w)
+                        C[w] = W[w];
+#pragma unroll
+                    for (int w = 0; w < RWL; ++w)
+                        if (w == wv)
+                            C[w] |= (u64)v << sh;
+                    C[RWL] += __ldg(key + v);
+                    store_record<RW, false>(p.pg, o++, C, 0);
+                }
+            }
+        }
+    }
+    if (!p.count)
+        cand = 0;
+    Acc acc;
+    acc.cyc = cnt;
+    acc.hash = hs;
+    acc.cand = cand;
+    acc.cyc_next = lcyc;
+    acc.cand_next = lcand;
+    acc.paths_next = lpaths;
+    flush(acc, p.sc);
+}
+
 // ---------------------------------------------------------------------------- keys, collect
 // nbrmask[u*n + z] |= 1 << k for the k-th neighbour w of u and every z ~ w (one warp per u;
 // lane k < deg(u) <= 32 owns neighbour k)
@@ -1831,6 +2065,39 @@ cudaError_t launch_wide(int which, const LaunchArgs &a, cudaStream_t st, int gri
                               : k_shard_filter_wide;
     const u64 per_block = which == 1 ? (u64)(kBlock / 32) * kWidePaths : (u64)kBlock;
     return run(f, grid_for(per_block, a.n_in, grid_cap), 0, st, a);
+}
+
+static KernelFn list_kernel(int which, int rwl, bool leaf)
+{
+    if (which == 0)
+        return rwl == 2 ? k_stage1_list<2> : rwl == 3 ? k_stage1_list<3> : nullptr;
+    if (which == 1) {
+        if (rwl == 2)
+            return leaf ? k_expand_list<2, true> : k_expand_list<2, false>;
+        if (rwl == 3)
+            return leaf ? k_expand_list<3, true> : k_expand_list<3, false>;
+        return nullptr;
+    }
+    return rwl == 2 ? k_shard_filter<3, false> : rwl == 3 ? k_shard_filter<4, false> : nullptr;
+}
+
+cudaError_t launch_list(int which, const LaunchArgs &a, int rwl, bool leaf, cudaStream_t st, int grid_cap)
+{
+    if (a.n_in == 0)
+        return cudaSuccess;
+    KernelFn f = list_kernel(which, rwl, leaf);
+    if (!f)
+        return cudaErrorInvalidValue;
+    return run(f, grid_for(kBlock, a.n_in, grid_cap), 0, st, a);
+}
+
+int max_blocks_per_sm_list(int which, int rwl)
+{
+    KernelFn f = list_kernel(which, rwl, false);
+    int nb = 1;
+    if (!f || cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, (const void *)f, kBlock, 0) != cudaSuccess || nb < 1)
+        nb = 1;
+    return nb;
 }
 
 int max_blocks_per_sm_wide(int which)

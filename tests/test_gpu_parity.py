@@ -254,18 +254,48 @@ def test_too_large_graph_rejected(ws):
 
 # ---------------------------------------------------------------- wide class (512 < n <= 2015)
 @pytest.mark.parametrize("K", [3, 4, 5, 6, 7, 8])
-def test_gnp2000_config3_capped(ws, K):
+@pytest.mark.parametrize("fmt", [1, 2])
+def test_gnp2000_config3_capped(ws, K, fmt):
     """BASELINE configs[3]: G(2000, 0.005) (seed inputs.GNP_SEED) per-length counts + set hash
-    with a length cap (full enumeration is infeasible: ~1e190 cycles)."""
+    with a length cap (full enumeration is infeasible: ~1e190 cycles), in both
+    frontier record formats (1 = blocked set, 2 = vertex list)."""
     g = I.gnp(2000, 0.005, I.GNP_SEED)
-    assert_same(gpu(g, ws, max_len=K), oracle.enumerate_cycles(*g, max_len=K, nthreads=NT))
+    if fmt == 2 and K < 4:
+        with pytest.raises(binding.CCError) as ei:
+            gpu(g, ws, max_len=K, record_format=2)
+        assert ei.value.kind == "CC_ERR_INVALID_ARGUMENT"
+        return
+    got = gpu(g, ws, max_len=K, record_format=fmt)
+    if K >= 4:
+        assert got["stats"]["record_bytes"] == (24 if fmt == 2 else 264)
+    assert_same(got, oracle.enumerate_cycles(*g, max_len=K, nthreads=NT))
 
 
 @pytest.mark.parametrize("n,p,K", [(513, 0.02, 7), (600, 0.01, 9), (1024, 0.006, 8), (1500, 0.004, 9),
                                    (2015, 0.003, 9)])
-def test_wide_class_sizes(ws, n, p, K):
+@pytest.mark.parametrize("fmt", [1, 0])
+def test_wide_class_sizes(ws, n, p, K, fmt):
     g = I.gnp(n, p, 4000 + n)
-    assert_same(gpu(g, ws, max_len=K), oracle.enumerate_cycles(*g, max_len=K, nthreads=NT))
+    assert_same(gpu(g, ws, max_len=K, record_format=fmt), oracle.enumerate_cycles(*g, max_len=K, nthreads=NT))
+
+
+@pytest.mark.parametrize("K", [4, 5, 6, 11, 12, 13, 14])
+def test_list_class_lengths(ws, K):
+    """Vertex-list records across the id-word boundaries (t = 4, 8, 12 vertices per path) and up
+    to the largest max_len the format takes (14: paths of 12 vertices, three id words)."""
+    g = I.grid(24, 24)  # n = 576 > 512: wide; Delta = 4; long chordless paths
+    got = gpu(g, ws, max_len=K, record_format=2)
+    assert got["stats"]["record_bytes"] == (24 if K <= 10 else 32)
+    assert_same(got, oracle.enumerate_cycles(*g, max_len=K, nthreads=NT))
+
+
+def test_list_class_rejects_what_it_cannot_hold(ws):
+    with pytest.raises(binding.CCError):
+        gpu(I.grid(24, 24), ws, max_len=15, record_format=2)  # 13-vertex paths
+    with pytest.raises(binding.CCError):
+        gpu(I.gnp(700, 0.06, 3), ws, max_len=6, record_format=2)  # Delta > 32
+    with pytest.raises(binding.CCError):
+        gpu(I.grid(10, 10), ws, max_len=6, record_format=2)  # n <= 512
 
 
 def test_wide_class_dense_and_grid(ws):
@@ -277,10 +307,12 @@ def test_wide_class_dense_and_grid(ws):
 
 
 @pytest.mark.parametrize("W", [2, 5])
-def test_wide_class_shards(ws, W):
+@pytest.mark.parametrize("fmt", [1, 2])
+def test_wide_class_shards(ws, W, fmt):
     g = I.gnp(2000, 0.005, I.GNP_SEED)
-    full = gpu(g, ws, max_len=7)
-    parts = [gpu(g, ws, max_len=7, shard_index=i, shard_count=W) for i in range(W)]
+    full = gpu(g, ws, max_len=7, record_format=fmt)
+    parts = [gpu(g, ws, max_len=7, shard_index=i, shard_count=W, record_format=fmt, min_shard_paths=256)
+             for i in range(W)]
     assert sum(p["counts"] for p in parts).tolist() == full["counts"].tolist()
     assert sum(p["set_hash"] for p in parts) % (1 << 64) == full["set_hash"]
     assert sum(p["paths_by_len"] for p in parts).tolist() == full["paths_by_len"].tolist()
@@ -292,9 +324,13 @@ def test_wide_class_chunked(ws):
     # 256 pages of 1024 records (~69 MB) cannot hold the ~12 M-path F_6, so levels are split; a page
     # must still fit one page of children (fan-out up to ~8 here), see DESIGN.md §5
     small = torch.empty(256 * 1024 * 264, dtype=torch.uint8, device="cuda")
-    got = binding.enumerate_cycles(*g, workspace=small, max_len=7)
+    got = binding.enumerate_cycles(*g, workspace=small, max_len=7, record_format=1)
     assert got["stats"]["chunks"] > got["stats"]["rounds"]
     assert_same(got, oracle.enumerate_cycles(*g, max_len=7, nthreads=NT))
+    small = torch.empty(32 << 20, dtype=torch.uint8, device="cuda")  # F_6 alone is 320 MB of lists
+    got = binding.enumerate_cycles(*g, workspace=small, max_len=8, record_format=2)
+    assert got["stats"]["chunks"] > got["stats"]["rounds"]
+    assert_same(got, oracle.enumerate_cycles(*g, max_len=8, nthreads=NT))
 
 
 def test_repeat_runs_deterministic(ws):
