@@ -43,6 +43,8 @@ WORKLOADS = {
                 "Erdos-Renyi G(2000, 0.005) (BASELINE configs[3]), cycles of <= 9 vertices"),
     "gnp2000k10": (lambda: inputs.gnp(2000, 0.005, inputs.GNP_SEED), 10,
                    "Erdos-Renyi G(2000, 0.005) (BASELINE configs[3]), cycles of <= 10 vertices"),
+    "gnp2000k11": (lambda: inputs.gnp(2000, 0.005, inputs.GNP_SEED), 11,
+                   "Erdos-Renyi G(2000, 0.005) (BASELINE configs[3]), cycles of <= 11 vertices"),
 }
 DEFAULT_WORKLOAD = "p10x10"
 
@@ -65,6 +67,7 @@ ORACLE_SAMPLE = {
     "grid8x10": dict(max_len=30),
     "gnp2000": dict(max_len=8),
     "gnp2000k10": dict(max_len=8),
+    "gnp2000k11": dict(max_len=8),
 }
 
 
@@ -296,8 +299,14 @@ def main():
     roofline = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                 "frac": achieved / peak, "traffic": traffic, "traffic_over_alg": traffic_ratio,
                 "peak_kind": peak_kind,
-                "kernel": "k_expand_blocked" if g[0] <= 512 else "k_expand_wide", "expand_share_of_step": t_expand / dev_ms if dev_ms else None,
+                "kernel": ("k_expand_blocked" if g[0] <= 512 else
+                           "k_expand_list" if st_last["record_format"] == 2 else "k_expand_wide"),
+                "expand_share_of_step": t_expand / dev_ms if dev_ms else None,
                 "bytes_alg_per_step": bytes_alg / args.steps}
+    if st_last["record_format"] == 2:
+        # vertex-list records (24 B) move so few bytes that HBM is not the bound: the time goes
+        # to random 4-byte reads of the neighbour-mask table in L2
+        roofline["note"] = "list class: L2-latency bound; HBM fraction reported for completeness"
     if args.workload in ALU_BOUND:
         # K_{a,b}: one expansion round in which every gate-passing candidate closes; no frontier
         # is written, so HBM is idle and the path is integer-ALU bound: the

@@ -124,6 +124,8 @@ typedef struct {
                                      children could not close within max_len) counted by the
                                      launch that created them and never written */
     uint64_t paths_written;       /* frontier records written by Stage 1 and Stage 2 */
+    uint64_t record_format;       /* frontier records used: 1 = blocked set (or bitmap S in
+                                     collect mode), 2 = vertex list (cc_options.record_format) */
 } cc_stats;
 
 /* Fills *opt with defaults (device -1, stream NULL, no cap, count-only, one shard). */

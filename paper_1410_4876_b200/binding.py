@@ -63,6 +63,7 @@ class cc_stats(ctypes.Structure):
         ("t_expand_ms", ctypes.c_double), ("t_stage1_ms", ctypes.c_double),
         ("t_labeling_ms", ctypes.c_double), ("t_wall_ms", ctypes.c_double),
         ("leaf_paths", ctypes.c_uint64), ("paths_written", ctypes.c_uint64),
+        ("record_format", ctypes.c_uint64),
     ]
 
 

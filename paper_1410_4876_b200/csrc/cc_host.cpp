@@ -546,6 +546,7 @@ static cc_status enumerate_impl(const cc_graph *cg, const cc_options *opt_in, cc
     const int rwl = list ? std::max<int>(2, (std::max<int>(3, (int)opt.max_len - 2) + 3) / 4) : 0;
     const u64 rec_bytes = list ? (u64)(rwl + 1) * 8 : (u64)cc::record_bytes(nw, mode, packed);
     S.record_bytes = rec_bytes;
+    S.record_format = list ? 2 : 1;
 
     // ---- frontier arena, split into pages of P = 2^lp records
     DevBuf ws_own;

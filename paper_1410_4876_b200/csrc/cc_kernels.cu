@@ -1842,28 +1842,40 @@ __global__ void __launch_bounds__(kBlock) k_expand_list(const LaunchArgs p)
         }
         const unsigned int ne = __popc(ext);
         const u64 off = block_reserve(ne, &p.sc->out_count, rs);
-        if (ne) {
-            if (off + ne > p.out_cap) {
+        // children <p, v>: the parent's list with v appended, keysum + key(v).  The warp's
+        // children fill [warp_base, warp_base + warp_total) round-robin -- round c holds the
+        // c-th child of every lane that has one, at consecutive positions -- so each store
+        // instruction writes consecutive records (coalesced) instead of one run per lane.
+        const int lane = threadIdx.x & 31;
+        const u64 wbase = __shfl_sync(FULL_MASK, off, 0);
+        const unsigned int wtot = __reduce_add_sync(FULL_MASK, ne);
+        if (wtot) {
+            if (lane == 0 && wbase + wtot > p.out_cap)
                 p.sc->err = 1;
-            } else {
-                // children <p, v>: the parent's list with v appended, keysum + key(v)
+            if (wbase + wtot <= p.out_cap) {
                 const int wv = t >> 2, sh = 16 * (t & 3);
-                u64 o = p.out_off + off;
+                u64 o = p.out_off + wbase;
                 uint32_t m = ext;
-                while (m) {
-                    const int k = __ffs(m) - 1;
-                    m &= m - 1;
-                    const uint32_t v = __ldg(col + rb + k);
-                    u64 C[RW];
+                for (;;) {
+                    const unsigned int has = __ballot_sync(FULL_MASK, m != 0u);
+                    if (!has)
+                        break;
+                    if (m) {
+                        const int k = __ffs(m) - 1;
+                        m &= m - 1;
+                        const uint32_t v = __ldg(col + rb + k);
+                        u64 C[RW];
 #pragma unroll
-                    for (int w = 0; w < RW; ++w)
-                        C[w] = W[w];
+                        for (int w = 0; w < RW; ++w)
+                            C[w] = W[w];
 #pragma unroll
-                    for (int w = 0; w < RWL; ++w)
-                        if (w == wv)
-                            C[w] |= (u64)v << sh;
-                    C[RWL] += __ldg(key + v);
-                    store_record<RW, false>(p.pg, o++, C, 0);
+                        for (int w = 0; w < RWL; ++w)
+                            if (w == wv)
+                                C[w] |= (u64)v << sh;
+                        C[RWL] += __ldg(key + v);
+                        store_record<RW, false>(p.pg, o + __popc(has & ((1u << lane) - 1u)), C, 0);
+                    }
+                    o += __popc(has);
                 }
             }
         }
