@@ -544,7 +544,7 @@ static cc_status enumerate_impl(const cc_graph *cg, const cc_options *opt_in, cc
                                                  std::to_string(cc::kListMaxLen));
     const bool list = opt.record_format == 2 || (opt.record_format == 0 && list_ok);
     const int rwl = list ? std::max<int>(2, (std::max<int>(3, (int)opt.max_len - 2) + 3) / 4) : 0;
-    const u64 rec_bytes = list ? (u64)(rwl + 1) * 8 : (u64)cc::record_bytes(nw, mode, packed);
+    const u64 rec_bytes = list ? (u64)(rwl + 2) * 8 : (u64)cc::record_bytes(nw, mode, packed);
     S.record_bytes = rec_bytes;
     S.record_format = list ? 2 : 1;
 

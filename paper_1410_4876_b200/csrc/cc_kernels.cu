@@ -1648,17 +1648,21 @@ __global__ void __launch_bounds__(kBlock) k_shard_filter_wide(const LaunchArgs p
 
 // ---------------------------------------------------------------------------- list class
 // Sparse wide graphs (count mode, 512 < n <= 2015, Delta <= 32, max_len <= 14).  A path is its
-// vertex list v1..vt (16-bit ids, four per word) plus keysum(p): 24 B for t <= 8 instead of a
-// 2000-bit blocked set.  One thread per path.  With the neighbour-mask table T = nbrmask
-// (bit k of T[u][z] = "k-th neighbour of u is adjacent to z"), the test of Alg. 3 lines 11-14
-// becomes 32-bit masks over the CSR row of vt (positions k, candidate v_k = col[row(vt) + k]):
-//   blocked = OR over the interior vertices x = v2..v_{t-1} of T[vt][x]   (v in B(p))
-//   Cand    = valid & {k : v_k > v2} & ~blocked
-//   Close   = Cand & T[vt][v1],   Ext = Cand & ~T[vt][v1]
-// (open rows suffice: the only path vertex in Adj(vt) is v_{t-1}, which is adjacent to the
-// interior v_{t-2}, or is v2 itself when t = 3 and fails the gate).  Last-level fusion: the
-// closers of the children lie in the row of v1, Z = {k : w_k > v2} & ~OR_{x in v2..vt} T[v1][x],
-// and child v closes through the positions T[v1][v] & Z.
+// vertex list v1..vt (16-bit ids, four per word: RWL words), one word holding Y(p), and
+// keysum(p): 32 B for t <= 8 instead of a 2000-bit blocked set.  One thread per path.  With
+// the neighbour-mask table T = nbrmask (bit k of T[u][z] = "k-th neighbour of u is adjacent
+// to z"), the test of Alg. 3 lines 11-14 becomes 32-bit masks over CSR rows:
+//   over the row of vt (candidates v_k = col[row(vt) + k]):
+//     blocked = OR over the interior vertices x = v2..v_{t-1} of T[vt][x]   (v in B(p))
+//     Ext     = valid & {k : v_k > v2} & ~blocked & ~T[vt][v1]
+//   (open rows suffice: the only path vertex in Adj(vt) is v_{t-1}, adjacent to the interior
+//   v_{t-2}, or v2 itself when t = 3, which fails the gate);
+//   over the row of v1 (the possible closing vertices w_k = col[row(v1) + k]), carried in the
+//   record and updated with one read per extension:
+//     Y(p)    = {k : w_k > v2} & ~{k : w_k in B(p)}        Y(<x,u,y>) = gate & ~T[x][u]
+//     Close(p) = Y(p) & T[v1][vt]                          (w ~ vt closes the cycle)
+//     Y(<p,v>) = Y(p) & ~T[v1][vt]                         (B grows by N[vt])
+// Last-level fusion: child v of p closes through Y(<p,v>) & T[v1][v], one read per child.
 __device__ __forceinline__ uint32_t list_id(const u64 *W, int i)
 {
     return (uint32_t)(W[i >> 2] >> (16 * (i & 3))) & 0xffffu;
@@ -1686,7 +1690,7 @@ __device__ __forceinline__ uint32_t low_mask(uint32_t k)  // bits 0..k-1 (k <= 3
 template <int RWL>
 __global__ void __launch_bounds__(kBlock) k_stage1_list(const LaunchArgs p)
 {
-    constexpr int RW = RWL + 1;
+    constexpr int RW = RWL + 2;
     __shared__ ReserveSmem rs;
     const int n = p.g.n, NW = p.g.nw;
     const u64 *__restrict__ adj = p.g.adj;
@@ -1734,7 +1738,11 @@ __global__ void __launch_bounds__(kBlock) k_stage1_list(const LaunchArgs p)
                     emit = (mix64(rkey) % p.root_stride) == p.root_offset;
                 }
                 W[0] = (u64)x | ((u64)u << 16) | ((u64)y << 32);  // <x, u, y>
-                W[RWL] = __ldg(key + x) + __ldg(key + u) + __ldg(key + y);
+                // Y(<x,u,y>) over the row of x: w > u and w not in N[u] (u itself fails w > u)
+                const uint32_t bx = __ldg(p.g.rowptr + x), dx = __ldg(p.g.rowptr + x + 1) - bx;
+                W[RWL] = low_mask(dx) & ~low_mask(row_rank(p.g.col, bx, dx, u)) &
+                         ~__ldg(p.g.nbrmask + (u64)x * n + u);
+                W[RWL + 1] = __ldg(key + x) + __ldg(key + u) + __ldg(key + y);
                 if (emit && p.filter)
                     emit = (shard_hash<RW>(W, 0) % p.shard_count) == p.shard_index;
             }
@@ -1753,7 +1761,7 @@ __global__ void __launch_bounds__(kBlock) k_stage1_list(const LaunchArgs p)
 template <int RWL, bool LEAF>
 __global__ void __launch_bounds__(kBlock) k_expand_list(const LaunchArgs p)
 {
-    constexpr int RW = RWL + 1;
+    constexpr int RW = RWL + 2;
     __shared__ ReserveSmem rs;
     __shared__ uint16_t s_deg[2048];
     const int t = (int)p.tlen;
@@ -1771,7 +1779,7 @@ __global__ void __launch_bounds__(kBlock) k_expand_list(const LaunchArgs p)
     for (u64 base = (u64)blockIdx.x * kBlock; base < p.n_in; base += stride) {
         const u64 r = base + threadIdx.x;
         u64 W[RW];
-        uint32_t ext = 0, rb = 0;
+        uint32_t ext = 0, rb = 0, Yc = 0;
         if (r < p.n_in) {
             const char *pp = page_ptr(p.pg, p.pg.in_pages[r >> p.pg.log_p]);
             const u64 slot = r & pmask;
@@ -1786,38 +1794,38 @@ __global__ void __launch_bounds__(kBlock) k_expand_list(const LaunchArgs p)
                 const u64 wq = q < 4 ? W[0] : (q < 8 || RWL < 3 ? W[1] : W[RWL - 1]);
                 vt = (uint32_t)(wq >> (16 * (q & 3))) & 0xffffu;
             }
-            const u64 ks = W[RWL];
-            rb = __ldg(rowptr + vt);
-            const uint32_t dt = s_deg[vt];
-            const u64 trow = (u64)vt * n;
-            uint32_t blocked = 0;
-#pragma unroll
-            for (int q = 1; q < 4 * RWL; ++q)
-                if (q < t - 1)
-                    blocked |= __ldg(T + trow + list_id(W, q));
-            const uint32_t a1m = __ldg(T + trow + v1);
-            const uint32_t cm = low_mask(dt) & ~low_mask(row_rank(col, rb, dt, v2)) & ~blocked;
-            uint32_t close = cm & a1m;
-            ext = p.emit ? (cm & ~a1m) : 0u;
-            if (p.count) {
-                cand += dt;
+            const uint32_t Y = (uint32_t)W[RWL];
+            const u64 ks = W[RWL + 1];
+            const u64 t1 = (u64)v1 * n;
+            const uint32_t tv = __ldg(T + t1 + vt);  // closers adjacent to vt
+            uint32_t close = Y & tv;
+            Yc = Y & ~tv;
+            uint32_t rb1 = 0;
+            if (close || (LEAF && Yc))
+                rb1 = __ldg(rowptr + v1);
+            if (p.count && close) {
                 cnt += __popc(close);
                 while (close) {
                     const int k = __ffs(close) - 1;
                     close &= close - 1;
-                    hs += mix64(ks + __ldg(key + __ldg(col + rb + k)));
+                    hs += mix64(ks + __ldg(key + __ldg(col + rb1 + k)));
                 }
+            }
+            rb = __ldg(rowptr + vt);
+            const uint32_t dt = s_deg[vt];
+            if (p.count)
+                cand += dt;
+            if (p.emit) {
+                const u64 trow = (u64)vt * n;
+                uint32_t blocked = __ldg(T + trow + v1);  // candidates adjacent to v1 close, not extend
+#pragma unroll
+                for (int q = 1; q < 4 * RWL; ++q)
+                    if (q < t - 1)
+                        blocked |= __ldg(T + trow + list_id(W, q));
+                ext = low_mask(dt) & ~low_mask(row_rank(col, rb, dt, v2)) & ~blocked;
             }
             if (LEAF) {
                 if (ext && p.count) {
-                    const uint32_t rb1 = __ldg(rowptr + v1), d1 = s_deg[v1];
-                    const u64 t1 = (u64)v1 * n;
-                    uint32_t blk1 = 0;
-#pragma unroll
-                    for (int q = 1; q < 4 * RWL; ++q)  // v2 .. vt
-                        if (q < t)
-                            blk1 |= __ldg(T + t1 + list_id(W, q));
-                    const uint32_t Z = low_mask(d1) & ~low_mask(row_rank(col, rb1, d1, v2)) & ~blk1;
                     uint32_t m = ext;
                     while (m) {
                         const int k = __ffs(m) - 1;
@@ -1825,7 +1833,7 @@ __global__ void __launch_bounds__(kBlock) k_expand_list(const LaunchArgs p)
                         const uint32_t v = __ldg(col + rb + k);
                         lpaths++;
                         lcand += s_deg[v];
-                        uint32_t c2 = Z ? (__ldg(T + t1 + v) & Z) : 0u;
+                        uint32_t c2 = Yc ? (__ldg(T + t1 + v) & Yc) : 0u;
                         if (c2) {
                             lcyc += __popc(c2);
                             const u64 kv = ks + __ldg(key + v);
@@ -1842,9 +1850,9 @@ __global__ void __launch_bounds__(kBlock) k_expand_list(const LaunchArgs p)
         }
         const unsigned int ne = __popc(ext);
         const u64 off = block_reserve(ne, &p.sc->out_count, rs);
-        // children <p, v>: the parent's list with v appended, keysum + key(v).  The warp's
-        // children fill [warp_base, warp_base + warp_total) round-robin -- round c holds the
-        // c-th child of every lane that has one, at consecutive positions -- so each store
+        // children <p, v>: the parent's list with v appended, Y(<p,v>), keysum + key(v).  The
+        // warp's children fill [warp_base, warp_base + warp_total) round-robin -- round c holds
+        // the c-th child of every lane that has one, at consecutive positions -- so each store
         // instruction writes consecutive records (coalesced) instead of one run per lane.
         const int lane = threadIdx.x & 31;
         const u64 wbase = __shfl_sync(FULL_MASK, off, 0);
@@ -1866,13 +1874,10 @@ __global__ void __launch_bounds__(kBlock) k_expand_list(const LaunchArgs p)
                         const uint32_t v = __ldg(col + rb + k);
                         u64 C[RW];
 #pragma unroll
-                        for (int w = 0; w < RW; ++w)
-                            C[w] = W[w];
-#pragma unroll
                         for (int w = 0; w < RWL; ++w)
-                            if (w == wv)
-                                C[w] |= (u64)v << sh;
-                        C[RWL] += __ldg(key + v);
+                            C[w] = W[w] | (w == wv ? (u64)v << sh : 0ull);
+                        C[RWL] = Yc;
+                        C[RWL + 1] = W[RWL + 1] + __ldg(key + v);
                         store_record<RW, false>(p.pg, o + __popc(has & ((1u << lane) - 1u)), C, 0);
                     }
                     o += __popc(has);
@@ -2090,7 +2095,7 @@ static KernelFn list_kernel(int which, int rwl, bool leaf)
             return leaf ? k_expand_list<3, true> : k_expand_list<3, false>;
         return nullptr;
     }
-    return rwl == 2 ? k_shard_filter<3, false> : rwl == 3 ? k_shard_filter<4, false> : nullptr;
+    return rwl == 2 ? k_shard_filter<4, false> : rwl == 3 ? k_shard_filter<5, false> : nullptr;
 }
 
 cudaError_t launch_list(int which, const LaunchArgs &a, int rwl, bool leaf, cudaStream_t st, int grid_cap)
