@@ -13,7 +13,10 @@ typedef unsigned long long u64;
 constexpr int kMaxWords = 8;           // n <= 512
 constexpr int kIdBits = 10;            // packed ids v1 | v2 << 10 | vt << 20 (n <= 1024)
 constexpr uint32_t kIdMask = (1u << kIdBits) - 1;
-constexpr int kBlock = 256;            // threads per CTA for every kernel
+#ifndef CC_BLOCK
+#define CC_BLOCK 256
+#endif
+constexpr int kBlock = CC_BLOCK;       // threads per CTA for every kernel
 // R: paths per thread per tile in k_expand_thread
 __host__ __device__ constexpr int expand_paths_per_thread(int nw) { return nw <= 4 ? 2 : 1; }
 constexpr int kMinLogPage = 10;        // pages hold >= kBlock * R records (one CTA tile)

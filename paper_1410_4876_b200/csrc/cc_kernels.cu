@@ -127,13 +127,16 @@ __device__ __forceinline__ u64 shard_hash(const u64 (&W)[RW], uint32_t id)
 // every thread of the block.  Returns this thread's first output index (relative to the
 // counter's origin).  Two barriers; callers that reserve repeatedly alternate two ReserveSmem
 // buffers (tile parity) so no third barrier is needed before the buffer is reused.
-struct ReserveSmem {
+template <int BS = kBlock>
+struct ReserveSmemT {
     u64 base;
     unsigned int total;
-    unsigned int warp[kBlock / 32];
+    unsigned int warp[BS / 32];
 };
+using ReserveSmem = ReserveSmemT<kBlock>;
 
-__device__ __forceinline__ u64 block_reserve2(unsigned int c, u64 *counter, ReserveSmem &sm)
+template <int BS = kBlock>
+__device__ __forceinline__ u64 block_reserve2(unsigned int c, u64 *counter, ReserveSmemT<BS> &sm)
 {
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
     unsigned int incl = c;
@@ -147,7 +150,7 @@ __device__ __forceinline__ u64 block_reserve2(unsigned int c, u64 *counter, Rese
         sm.warp[wid] = incl;
     __syncthreads();
     if (wid == 0) {
-        const unsigned int w = lane < kBlock / 32 ? sm.warp[lane] : 0u;
+        const unsigned int w = lane < BS / 32 ? sm.warp[lane] : 0u;
         unsigned int wi = w;
 #pragma unroll
         for (int o = 1; o < 32; o <<= 1) {
@@ -155,9 +158,9 @@ __device__ __forceinline__ u64 block_reserve2(unsigned int c, u64 *counter, Rese
             if (lane >= o)
                 wi += v;
         }
-        if (lane < kBlock / 32)
+        if (lane < BS / 32)
             sm.warp[lane] = wi - w;
-        if (lane == kBlock / 32 - 1) {
+        if (lane == BS / 32 - 1) {
             sm.total = wi;
             sm.base = wi ? atomicAdd(counter, (u64)wi) : 0ull;
         }
@@ -187,7 +190,8 @@ __device__ __forceinline__ void lds_row(const u64 *base, uint32_t v, u64 (&r)[NW
 // *ticket.  That lane calls reserve_publish(ticket) later, after independent work, so the
 // atomic's round trip overlaps that work instead of stalling every warp at a barrier; the base
 // is visible to all threads after the caller's next barrier.
-__device__ __forceinline__ unsigned int reserve_begin(unsigned int c, u64 *counter, ReserveSmem &sm, u64 *ticket)
+template <int BS = kBlock>
+__device__ __forceinline__ unsigned int reserve_begin(unsigned int c, u64 *counter, ReserveSmemT<BS> &sm, u64 *ticket)
 {
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
     unsigned int incl = c;
@@ -201,7 +205,7 @@ __device__ __forceinline__ unsigned int reserve_begin(unsigned int c, u64 *count
         sm.warp[wid] = incl;
     __syncthreads();
     if (wid == 0) {
-        const unsigned int w = lane < kBlock / 32 ? sm.warp[lane] : 0u;
+        const unsigned int w = lane < BS / 32 ? sm.warp[lane] : 0u;
         unsigned int wi = w;
 #pragma unroll
         for (int o = 1; o < 32; o <<= 1) {
@@ -209,9 +213,9 @@ __device__ __forceinline__ unsigned int reserve_begin(unsigned int c, u64 *count
             if (lane >= o)
                 wi += v;
         }
-        if (lane < kBlock / 32)
+        if (lane < BS / 32)
             sm.warp[lane] = wi - w;
-        if (lane == kBlock / 32 - 1) {
+        if (lane == BS / 32 - 1) {
             sm.total = wi;
             *ticket = wi ? atomicAdd(counter, (u64)wi) : 0ull;
         }
@@ -220,12 +224,14 @@ __device__ __forceinline__ unsigned int reserve_begin(unsigned int c, u64 *count
     return sm.warp[wid] + (incl - c);
 }
 
-__device__ __forceinline__ bool is_ticket_lane() { return threadIdx.x == kBlock / 32 - 1; }
+template <int BS = kBlock>
+__device__ __forceinline__ bool is_ticket_lane() { return threadIdx.x == BS / 32 - 1; }
 
 // single-buffer form: a third barrier protects sm before its next use
-__device__ __forceinline__ u64 block_reserve(unsigned int c, u64 *counter, ReserveSmem &sm)
+template <int BS = kBlock>
+__device__ __forceinline__ u64 block_reserve(unsigned int c, u64 *counter, ReserveSmemT<BS> &sm)
 {
-    const u64 r = block_reserve2(c, counter, sm);
+    const u64 r = block_reserve2<BS>(c, counter, sm);
     __syncthreads();
     return r;
 }
@@ -312,10 +318,11 @@ struct Acc {
     u64 cyc = 0, hash = 0, cand = 0, cyc_next = 0, cand_next = 0, paths_next = 0;
 };
 
+template <int BS = kBlock>
 __device__ __forceinline__ void flush(Acc a, Scratch *sc)
 {
     constexpr int K = 6;
-    __shared__ u64 red[K][kBlock / 32];
+    __shared__ u64 red[K][BS / 32];
     u64 v[K] = {a.cyc, a.hash, a.cand, a.cyc_next, a.cand_next, a.paths_next};
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
 #pragma unroll
@@ -329,7 +336,7 @@ __device__ __forceinline__ void flush(Acc a, Scratch *sc)
     __syncthreads();
     if (threadIdx.x < K) {
         u64 s = 0;
-        for (int i = 0; i < kBlock / 32; ++i)
+        for (int i = 0; i < BS / 32; ++i)
             s += red[threadIdx.x][i];
         // the six counters are consecutive u64 fields of Scratch starting at `cycles`
         static_assert(offsetof(Scratch, paths_next) - offsetof(Scratch, cycles) == 5 * sizeof(u64), "Scratch layout");
@@ -338,13 +345,14 @@ __device__ __forceinline__ void flush(Acc a, Scratch *sc)
     }
 }
 
+template <int BS = kBlock>
 __device__ __forceinline__ void flush_accum(u64 cnt, u64 hs, u64 cand, Scratch *sc)
 {
     Acc a;
     a.cyc = cnt;
     a.hash = hs;
     a.cand = cand;
-    flush(a, sc);
+    flush<BS>(a, sc);
 }
 
 // Graph tables staged in shared memory: adjacency bit rows (n*NW words), keys (n words) and,
@@ -526,22 +534,29 @@ __global__ void __launch_bounds__(kBlock) k_stage1(const LaunchArgs p)
 #define CC_CHILD_CAP_X4 8
 #endif
 constexpr int kStages = CC_STAGES;
+#ifndef CC_EB_BLOCK
+#define CC_EB_BLOCK 128
+#endif
+constexpr int kEBBlock = CC_EB_BLOCK;
+#ifndef CC_EB_MINB
+#define CC_EB_MINB 3  // register bound of k_expand_blocked (NW <= 2): at least 3 resident CTAs
+#endif  // threads per CTA of k_expand_blocked (smaller CTAs: barriers span fewer warps)
 constexpr int kChildCapX4 = CC_CHILD_CAP_X4;  // child list capacity = kChildCapX4/4 per path slot
 
 template <int NW, bool PACK>
 __host__ __device__ constexpr size_t blocked_stage_bytes()
 {
-    return (size_t)kBlock * expand_paths_per_thread(NW) * ((NW + 1) * 8 + (PACK ? 0 : 4));
+    return (size_t)kEBBlock * expand_paths_per_thread(NW) * ((NW + 1) * 8 + (PACK ? 0 : 4));
 }
 
 // MAXCH > 0: every path has at most MAXCH children (Delta - 1, host-checked), so the staging of
 // children is unrolled into MAXCH predicated steps instead of a divergent per-bit loop.
 template <int NW, int MAXCH, bool PACK, bool LEAF>
-__global__ void __launch_bounds__(kBlock, NW <= 2 ? 3 : 2) k_expand_blocked(const LaunchArgs p)
+__global__ void __launch_bounds__(kEBBlock, NW <= 2 ? CC_EB_MINB : 2) k_expand_blocked(const LaunchArgs p)
 {
     constexpr int RW = NW + 1;
     constexpr int R = expand_paths_per_thread(NW);
-    constexpr int kTile = kBlock * R;
+    constexpr int kTile = kEBBlock * R;
     constexpr uint32_t kStageBytes = (uint32_t)blocked_stage_bytes<NW, PACK>();
     constexpr uint32_t kChildCap = kChildCapX4 * kTile / 4;  // overflow falls back to per-thread appends
     extern __shared__ __align__(128) u64 smem[];
@@ -556,7 +571,7 @@ __global__ void __launch_bounds__(kBlock, NW <= 2 ? 3 : 2) k_expand_blocked(cons
     u64 *s_par = s_above + p.g.n * NW;                    // [kTile][PW]
     uint32_t *s_pid = (uint32_t *)(s_par + kTile * PW);   // [kTile] (unpacked ids only)
     uint32_t *s_child = s_pid + (PACK ? 0 : kTile);       // [kChildCap]
-    __shared__ ReserveSmem rs[2];
+    __shared__ ReserveSmemT<kEBBlock> rs[2];
     __shared__ __align__(8) u64 bar[kStages];
 
     const uint32_t idb = PACK ? p.idb : (uint32_t)kIdBits;
@@ -590,11 +605,11 @@ __global__ void __launch_bounds__(kBlock, NW <= 2 ? 3 : 2) k_expand_blocked(cons
     }
     // closed rows N[v] = Adj(v) | {v} in s_adj: vt and v1 always lie in B, so Cand/Close/Ext are
     // unchanged, and the children's blocked set B | N[vt] is a plain OR
-    for (int i = threadIdx.x; i < p.g.n * NW; i += kBlock) {
+    for (int i = threadIdx.x; i < p.g.n * NW; i += kEBBlock) {
         s_above[i] = above_word((uint32_t)(i / NW), i % NW);
         s_adj[i] = p.g.adj[i] | bit_in_word(i % NW, (uint32_t)(i / NW));
     }
-    for (int i = threadIdx.x; i < p.g.n; i += kBlock)
+    for (int i = threadIdx.x; i < p.g.n; i += kEBBlock)
         s_key[i] = p.g.key[i];
     __syncthreads();
 
@@ -616,7 +631,7 @@ __global__ void __launch_bounds__(kBlock, NW <= 2 ? 3 : 2) k_expand_blocked(cons
         bool valid[R];
 #pragma unroll
         for (int i = 0; i < R; ++i) {
-            const int j = threadIdx.x + kBlock * i;
+            const int j = threadIdx.x + kEBBlock * i;
 #pragma unroll
             for (int w = 0; w < RW; ++w)
                 W[i][w] = ((const u64 *)buf)[w * kTile + j];
@@ -708,7 +723,7 @@ __global__ void __launch_bounds__(kBlock, NW <= 2 ? 3 : 2) k_expand_blocked(cons
         }
         // every thread has read stage st (the reservation starts with a barrier) -> refill it
         u64 ticket = 0;
-        const unsigned int loc0 = reserve_begin(ne, &p.sc->out_count, rs[k & 1], &ticket);
+        const unsigned int loc0 = reserve_begin<kEBBlock>(ne, &p.sc->out_count, rs[k & 1], &ticket);
         if (threadIdx.x == 0 && k + kStages < my_tiles) {
             asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
             issue(k + kStages);
@@ -728,7 +743,7 @@ __global__ void __launch_bounds__(kBlock, NW <= 2 ? 3 : 2) k_expand_blocked(cons
                     any |= ext[i][w] != 0ull;
                 if (!any)
                     continue;
-                const uint32_t slot = threadIdx.x + kBlock * i;
+                const uint32_t slot = threadIdx.x + kEBBlock * i;
                 const uint32_t vt = id[i] >> (2 * idb);
                 u64 ar[NW];
                 lds_row<NW>(s_adj, vt, ar);
@@ -767,7 +782,7 @@ __global__ void __launch_bounds__(kBlock, NW <= 2 ? 3 : 2) k_expand_blocked(cons
                 }
             }
         }
-        if (is_ticket_lane())
+        if (is_ticket_lane<kEBBlock>())
             rs[k & 1].base = ticket;  // the atomic's result is needed only now
         __syncthreads();
         const u64 tile_base = rs[k & 1].base;  // first output position of this CTA tile
@@ -814,7 +829,7 @@ __global__ void __launch_bounds__(kBlock, NW <= 2 ? 3 : 2) k_expand_blocked(cons
             const uint32_t split = (uint32_t)(pmask + 1 - s0);
             char *pp0 = page_ptr(p.pg, p.pg.out_pages[o0 >> p.pg.log_p]);
             char *pp1 = split < total ? page_ptr(p.pg, p.pg.out_pages[(o0 >> p.pg.log_p) + 1]) : pp0;
-            for (unsigned int j = threadIdx.x; j < total; j += kBlock) {
+            for (unsigned int j = threadIdx.x; j < total; j += kEBBlock) {
                 const uint32_t e = s_child[j];
                 const uint32_t slot = e & 0xffffu;
                 uint32_t v;
@@ -876,7 +891,7 @@ __global__ void __launch_bounds__(kBlock, NW <= 2 ? 3 : 2) k_expand_blocked(cons
     a.cyc_next = leaf_cyc;
     a.cand_next = leaf_cand;
     a.paths_next = leaf_paths;
-    flush(a, p.sc);
+    flush<kEBBlock>(a, p.sc);
 }
 
 // ---------------------------------------------------------------------------- Stage 2, S-mode
@@ -1687,17 +1702,22 @@ __device__ __forceinline__ uint32_t low_mask(uint32_t k)  // bits 0..k-1 (k <= 3
     return k >= 32 ? 0xffffffffu : ((1u << k) - 1u);
 }
 
+#ifndef CC_LIST_BLOCK
+#define CC_LIST_BLOCK 512
+#endif
+constexpr int kListBlock = CC_LIST_BLOCK;  // threads per CTA of the list kernels
+
 template <int RWL>
-__global__ void __launch_bounds__(kBlock) k_stage1_list(const LaunchArgs p)
+__global__ void __launch_bounds__(kListBlock) k_stage1_list(const LaunchArgs p)
 {
     constexpr int RW = RWL + 2;
-    __shared__ ReserveSmem rs;
+    __shared__ ReserveSmemT<kListBlock> rs;
     const int n = p.g.n, NW = p.g.nw;
     const u64 *__restrict__ adj = p.g.adj;
     const u64 *__restrict__ key = p.g.key;
     u64 cnt = 0, hs = 0;
-    const u64 stride = (u64)gridDim.x * kBlock;
-    for (u64 base = (u64)blockIdx.x * kBlock; base < p.n_in; base += stride) {
+    const u64 stride = (u64)gridDim.x * kListBlock;
+    for (u64 base = (u64)blockIdx.x * kListBlock; base < p.n_in; base += stride) {
         const u64 r = base + threadIdx.x;
         unsigned int emit = 0;
         u64 W[RW];
@@ -1747,7 +1767,7 @@ __global__ void __launch_bounds__(kBlock) k_stage1_list(const LaunchArgs p)
                     emit = (shard_hash<RW>(W, 0) % p.shard_count) == p.shard_index;
             }
         }
-        const u64 off = block_reserve(emit, &p.sc->out_count, rs);
+        const u64 off = block_reserve<kListBlock>(emit, &p.sc->out_count, rs);
         if (emit) {
             if (off >= p.out_cap)
                 p.sc->err = 1;
@@ -1755,14 +1775,14 @@ __global__ void __launch_bounds__(kBlock) k_stage1_list(const LaunchArgs p)
                 store_record<RW, false>(p.pg, p.out_off + off, W, 0);
         }
     }
-    flush_accum(cnt, hs, 0, p.sc);
+    flush_accum<kListBlock>(cnt, hs, 0, p.sc);
 }
 
 template <int RWL, bool LEAF>
-__global__ void __launch_bounds__(kBlock) k_expand_list(const LaunchArgs p)
+__global__ void __launch_bounds__(kListBlock) k_expand_list(const LaunchArgs p)
 {
     constexpr int RW = RWL + 2;
-    __shared__ ReserveSmem rs;
+    __shared__ ReserveSmemT<kListBlock> rs;
     __shared__ uint16_t s_deg[2048];
     const int t = (int)p.tlen;
     const uint32_t n = (uint32_t)p.g.n;
@@ -1770,13 +1790,13 @@ __global__ void __launch_bounds__(kBlock) k_expand_list(const LaunchArgs p)
     const uint32_t *__restrict__ col = p.g.col;
     const uint32_t *__restrict__ rowptr = p.g.rowptr;
     const u64 *__restrict__ key = p.g.key;
-    for (uint32_t v = threadIdx.x; v < n; v += kBlock)
+    for (uint32_t v = threadIdx.x; v < n; v += kListBlock)
         s_deg[v] = (uint16_t)(rowptr[v + 1] - rowptr[v]);
     __syncthreads();
     const u64 pmask = (1ull << p.pg.log_p) - 1;
     u64 cnt = 0, hs = 0, cand = 0, lpaths = 0, lcand = 0, lcyc = 0;
-    const u64 stride = (u64)gridDim.x * kBlock;
-    for (u64 base = (u64)blockIdx.x * kBlock; base < p.n_in; base += stride) {
+    const u64 stride = (u64)gridDim.x * kListBlock;
+    for (u64 base = (u64)blockIdx.x * kListBlock; base < p.n_in; base += stride) {
         const u64 r = base + threadIdx.x;
         u64 W[RW];
         uint32_t ext = 0, rb = 0, Yc = 0;
@@ -1849,7 +1869,7 @@ __global__ void __launch_bounds__(kBlock) k_expand_list(const LaunchArgs p)
             }
         }
         const unsigned int ne = __popc(ext);
-        const u64 off = block_reserve(ne, &p.sc->out_count, rs);
+        const u64 off = block_reserve<kListBlock>(ne, &p.sc->out_count, rs);
         // children <p, v>: the parent's list with v appended, Y(<p,v>), keysum + key(v).  The
         // warp's children fill [warp_base, warp_base + warp_total) round-robin -- round c holds
         // the c-th child of every lane that has one, at consecutive positions -- so each store
@@ -1894,7 +1914,7 @@ __global__ void __launch_bounds__(kBlock) k_expand_list(const LaunchArgs p)
     acc.cyc_next = lcyc;
     acc.cand_next = lcand;
     acc.paths_next = lpaths;
-    flush(acc, p.sc);
+    flush<kListBlock>(acc, p.sc);
 }
 
 // ---------------------------------------------------------------------------- keys, collect
@@ -1996,7 +2016,7 @@ static size_t blocked_ring_bytes(int nw, bool packed)
 size_t expand_smem(Mode m, int nw, int n, bool packed)
 {
     if (m == Mode::B) {
-        const size_t tile = (size_t)kBlock * expand_paths_per_thread(nw);
+        const size_t tile = (size_t)kEBBlock * expand_paths_per_thread(nw);
         return blocked_ring_bytes(nw, packed) + ((size_t)n * 2 * nw + ((n + 1) & ~1)) * sizeof(u64) +
                tile * (2 * nw + 1) * 8 +
                (packed ? 0 : tile * 4) + (size_t)kChildCapX4 * tile;
@@ -2014,12 +2034,13 @@ static cudaError_t set_smem(KernelFn f, size_t smem)
     return cudaSuccess;
 }
 
-static cudaError_t run(KernelFn f, unsigned int grid, size_t smem, cudaStream_t st, const LaunchArgs &a)
+static cudaError_t run(KernelFn f, unsigned int grid, size_t smem, cudaStream_t st, const LaunchArgs &a,
+                       int block = kBlock)
 {
     cudaError_t e = set_smem(f, smem);
     if (e != cudaSuccess)
         return e;
-    f<<<grid, kBlock, smem, st>>>(a);
+    f<<<grid, block, smem, st>>>(a);
     return cudaGetLastError();
 }
 
@@ -2105,14 +2126,16 @@ cudaError_t launch_list(int which, const LaunchArgs &a, int rwl, bool leaf, cuda
     KernelFn f = list_kernel(which, rwl, leaf);
     if (!f)
         return cudaErrorInvalidValue;
-    return run(f, grid_for(kBlock, a.n_in, grid_cap), 0, st, a);
+    const int block = which == 2 ? kBlock : kListBlock;  // the shard filter is the generic kernel
+    return run(f, grid_for(block, a.n_in, grid_cap), 0, st, a, block);
 }
 
 int max_blocks_per_sm_list(int which, int rwl)
 {
     KernelFn f = list_kernel(which, rwl, false);
     int nb = 1;
-    if (!f || cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, (const void *)f, kBlock, 0) != cudaSuccess || nb < 1)
+    const int block = which == 2 ? kBlock : kListBlock;
+    if (!f || cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, (const void *)f, block, 0) != cudaSuccess || nb < 1)
         nb = 1;
     return nb;
 }
@@ -2146,10 +2169,11 @@ cudaError_t launch_expand(const LaunchArgs &a, Mode m, ExpandVariant v, cudaStre
         return cudaErrorInvalidValue;
     u64 per_block = kBlock;
     if (m == Mode::B)
-        per_block = (u64)kBlock * expand_paths_per_thread(a.g.nw);
+        per_block = (u64)kEBBlock * expand_paths_per_thread(a.g.nw);
     else if (v == ExpandVariant::Warp)
         per_block = kBlock / 32;
-    return run(f, grid_for(per_block, a.n_in, grid_cap), expand_smem(m, a.g.nw, a.g.n, a.packed != 0), st, a);
+    return run(f, grid_for(per_block, a.n_in, grid_cap), expand_smem(m, a.g.nw, a.g.n, a.packed != 0), st, a,
+               m == Mode::B ? kEBBlock : kBlock);
 }
 
 cudaError_t launch_shard_filter(const LaunchArgs &a, Mode m, cudaStream_t st, int grid_cap)
@@ -2207,10 +2231,12 @@ int max_blocks_per_sm(int which, Mode m, int nw, bool packed, size_t smem)
     if (!f)
         return 1;
     const size_t sm = which == 3 ? 0 : smem;
+    // the B-mode expansion kernel runs kEBBlock-thread CTAs (grid sizes are in CTAs)
+    const int block = (m == Mode::B && (which == 1 || which == 2 || which == 4)) ? kEBBlock : kBlock;
     int nb = 1;
     if (set_smem(f, sm) != cudaSuccess)
         return 1;
-    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, (const void *)f, kBlock, sm) != cudaSuccess || nb < 1)
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, (const void *)f, block, sm) != cudaSuccess || nb < 1)
         nb = 1;
     return nb;
 }
