@@ -267,8 +267,12 @@ def main():
     # ---- combine across ranks: counts + hash (SUM, the only data exchange) and time (MAX)
     cyc_local = int(counts.sum())
     paths_local = int(paths.sum())
+    per_rank = None
     if world > 1:
         from paper_1410_4876_b200 import dist as D
+        # per-rank device time and paths (the imbalance of the static partition)
+        per_rank = [{"rank": i, "ms_per_step": v[0] / args.steps, "paths": int(v[1])}
+                    for i, v in enumerate(D.gather_per_rank([dev_ms, paths_local], device=comm_dev))]
         dev_ms = D.max_over_ranks(dev_ms, device=comm_dev)
         counts, h, paths_total = D.combine_shards(counts, h, paths_local, device=comm_dev)
     else:
@@ -344,7 +348,9 @@ def main():
             from paper_1410_4876_b200 import dist as D
             el = D.max_over_ranks(el, device=comm_dev)
         e2e = {"value": cycles_total / (el / ne), "unit": UNIT, "h2d_bytes_per_step": h2d // ne,
-               "d2h_bytes_per_step": d2h // ne, "ms_per_step": 1e3 * el / ne}
+               "d2h_bytes_per_step": d2h // ne, "ms_per_step": 1e3 * el / ne,
+               # t_proc = host labelling + device time (the paper's T_par-proc)
+               "t_labeling_ms": s2["t_labeling_ms"], "t_proc_ms": s2["t_labeling_ms"] + ms_per_step}
 
     if rank == 0:
         cpu = None
@@ -364,6 +370,7 @@ def main():
             "set_hash": f"{h:#018x}", "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e,
             "gpu_launches": launches, "clocks": clk.summary(),
             "frontier_sizes": {str(t): int(v) for t, v in enumerate(paths) if v} if world == 1 else None,
+            "per_rank": per_rank,
             "per_step": {"chunks": st_last["chunks"], "rounds": st_last["rounds"],
                          "peak_arena_records": st_last["peak_arena_records"],
                          "t_stage1_ms": st_last["t_stage1_ms"], "t_expand_ms": st_last["t_expand_ms"]},

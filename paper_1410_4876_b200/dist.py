@@ -43,3 +43,17 @@ def max_over_ranks(x: float, device=None, group=None) -> float:
         t = t.to(device)
     dist.all_reduce(t, op=dist.ReduceOp.MAX, group=group)
     return float(t.item())
+
+
+def gather_per_rank(values, device=None, group=None):
+    """All ranks' small float vectors (e.g. [device ms, paths]) for the imbalance report,
+    SURVEY §8(e) -- reporting only, not on the data path."""
+    import torch
+    import torch.distributed as dist
+
+    t = torch.tensor([float(v) for v in values], dtype=torch.float64)
+    if device is not None:
+        t = t.to(device)
+    out = [torch.zeros_like(t) for _ in range(dist.get_world_size(group))]
+    dist.all_gather(out, t, group=group)
+    return [[float(x) for x in o.cpu().tolist()] for o in out]

@@ -31,8 +31,9 @@ def _worker(rank, world, port, graph_name, out_q):
     r = oracle.enumerate_cycles(*g, root_stride=world, root_offset=rank)
     counts, h, paths = D.combine_shards(r["counts"], r["set_hash"], int(r["paths_by_len"].sum()))
     t = D.max_over_ranks(float(rank + 1))
+    pr = D.gather_per_rank([float(rank + 1), float(int(r["paths_by_len"].sum()))])
     if rank == 0:
-        out_q.put((counts.tolist(), h, paths, t))
+        out_q.put((counts.tolist(), h, paths, t, pr))
     dist.barrier()
     dist.destroy_process_group()
 
@@ -49,7 +50,7 @@ def test_gloo_combine_equals_unsharded(world, graph_name):
     procs = [ctx.Process(target=_worker, args=(r, world, port, graph_name, q)) for r in range(world)]
     for p in procs:
         p.start()
-    counts, h, paths, t = q.get(timeout=120)
+    counts, h, paths, t, pr = q.get(timeout=120)
     for p in procs:
         p.join(timeout=60)
         assert p.exitcode == 0
@@ -58,6 +59,9 @@ def test_gloo_combine_equals_unsharded(world, graph_name):
     assert h == full["set_hash"]
     assert paths == int(full["paths_by_len"].sum())
     assert t == float(world)
+    # per-rank report (bench.py "per_rank"): every rank's row, in rank order, summing to the whole
+    assert [row[0] for row in pr] == [float(r + 1) for r in range(world)]
+    assert sum(row[1] for row in pr) == paths
 
 
 def test_hash_wraps_mod_2_64():
