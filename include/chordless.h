@@ -63,9 +63,11 @@ typedef struct {
                                  PAPER.md:419); 1 = also keep every cycle for cc_fetch_cycles */
     uint32_t shard_index;     /* this rank's share of the search tree, 0 <= index < count */
     uint32_t shard_count;     /* 1 = everything.  Shards partition the paths of the first
-                                 frontier level with >= 1024*count paths by a content hash;
-                                 earlier levels are counted by shard 0 only.  The sums over
-                                 shards equal the unsharded result exactly (counts and hash). */
+                                 frontier level with >= min_shard_paths * count paths (default
+                                 2^20 per shard) by a content hash of the record; earlier levels
+                                 run on every shard and are counted by shard 0 only.  The sums
+                                 over shards equal the unsharded result exactly (counts, hash,
+                                 paths per level, candidates). */
     uint64_t root_stride;     /* root sample: keep triplet <x,u,y> iff
                                  mix(x<<42 | u<<21 | y) % root_stride == root_offset
                                  (original ids); 0 or 1 = all roots.  Triangles are counted
@@ -152,9 +154,18 @@ cc_status cc_graph_labels(const cc_graph *g, int32_t *labels);
 
 /*
  * Enumerate every chordless cycle of g exactly once on the GPU.
- * Size classes: n <= 512 (records of <= 8 bitmap words; count and collect mode) and
- * 512 < n <= 2015 (wide records of <= 32 words, one warp per path; count mode only).  Larger
- * graphs, and collect mode above n = 512, fail with CC_ERR_TOO_LARGE.  Errors: CC_ERR_NO_DEVICE, CC_ERR_CUDA, CC_ERR_CAPACITY,
+ * Size classes:
+ *   n <= 512: bitset records of <= 8 words; count and collect mode;
+ *   512 < n <= 2015: count mode only; blocked-set records of <= 32 words (one warp per
+ *     path), or vertex-list records (one thread per path; max degree <= 32 and
+ *     4 <= max_len <= 14; see cc_options.record_format).
+ * Larger graphs, and collect mode above n = 512, fail with CC_ERR_TOO_LARGE.
+ * With max_len, count mode fuses the last level: the paths of max_len - 1 vertices are
+ * counted (with their closures) by the launch that creates them and are never written
+ * (cc_stats.leaf_paths).  Results do not depend on the record format, the workspace size,
+ * the chunking or the shard count.
+ * Errors: CC_ERR_NO_DEVICE, CC_ERR_CUDA, CC_ERR_CAPACITY (workspace too small to make
+ * progress: one page of the deepest level needs more output than the free pages hold),
  * CC_ERR_INVALID_ARGUMENT (bad options).  On success *out owns the counts, set hash,
  * per-level statistics and (collect mode) the cycles in device memory.
  */
@@ -169,7 +180,7 @@ cc_status cc_enumerate(const cc_graph *g, const cc_options *opt, cc_result **out
 cc_status cc_count_by_length(const cc_result *r, uint64_t *counts, size_t cap, size_t *n_lengths,
                              uint64_t *set_hash);
 
-/* paths[t] = |F_t|, paths of t vertices scanned by Stage 2 (t = 0..n); sizes as above.
+/* paths[t] = |F_t|, paths of t vertices created (t = 0..n; the oracle's visited paths); sizes as above.
  * This is the |T| evolution of the paper's Fig. 4. */
 cc_status cc_paths_by_length(const cc_result *r, uint64_t *paths, size_t cap, size_t *n_lengths);
 
