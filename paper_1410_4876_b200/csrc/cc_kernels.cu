@@ -672,12 +672,18 @@ __global__ void __launch_bounds__(kEBBlock, NW <= 2 ? CC_EB_MINB : 2) k_expand_b
                 const u64 ks = W[i][NW];
 #pragma unroll
                 for (int w = 0; w < NW; ++w) {
-                    u64 m = close[w];
+                    const u64 m = close[w];
                     cnt += __popcll(m);
-                    while (m) {
-                        const int b = __ffsll((long long)m) - 1;
-                        m &= m - 1;
-                        hs += mix64(ks + s_key[64 * w + b]);
+                    // 32-bit halves: cheaper bit extraction on 32-bit lanes (K_{a,b}: ~100
+                    // closures per path, each dominated by the 64-bit mix)
+#pragma unroll
+                    for (int h = 0; h < 2; ++h) {
+                        uint32_t mm = (uint32_t)(m >> (32 * h));
+                        while (mm) {
+                            const int b = __ffs(mm) - 1;
+                            mm &= mm - 1;
+                            hs += mix64(ks + s_key[64 * w + 32 * h + b]);
+                        }
                     }
                 }
             }
