@@ -248,24 +248,34 @@ def cc_num_stored_cycles(r: Result) -> int:
     return int(k.value)
 
 
-def cc_fetch_cycles(r: Result, first: int = 0, max_cycles: int | None = None):
-    """Returns (vertices int32[], offsets uint64[k+1]) for cycles [first, first+k)."""
+def cc_fetch_cycles(r: Result, first: int = 0, max_cycles: int | None = None, max_len: int | None = None):
+    """Returns (vertices int32[], offsets uint64[k+1]) for cycles [first, first+k).
+
+    The vertex buffer is sized from the longest stored cycle (``max_len``, default: the
+    largest k with counts[k] > 0), so one library call fetches the batch; the two-call sizing
+    protocol of the C ABI is the fallback."""
     lib = load()
     total = cc_num_stored_cycles(r)
     if max_cycles is None:
         max_cycles = max(total - first, 0)
-    offsets = np.zeros(max_cycles + 1, dtype=np.uint64)
+    k = min(max_cycles, max(total - first, 0))
+    if max_len is None:
+        counts, _ = cc_count_by_length(r)
+        nz = np.nonzero(counts)[0]
+        max_len = int(nz[-1]) if len(nz) else 0
+    offsets = np.empty(max_cycles + 1, dtype=np.uint64)
+    verts = np.empty(max(k * max_len, 1), dtype=np.int32)
     nf = ctypes.c_uint64()
-    st = lib.cc_fetch_cycles(r.handle, first, max_cycles, None, 0, _ptr(offsets), ctypes.byref(nf))
-    if st == 8:  # BUFFER_TOO_SMALL: offsets tell the size
-        k = min(max_cycles, max(total - first, 0))
-        verts = np.zeros(max(int(offsets[k]), 1), dtype=np.int32)
-        _check(lib.cc_fetch_cycles(r.handle, first, max_cycles, _ptr(verts), verts.size,
-                                   _ptr(offsets), ctypes.byref(nf)))
-    else:
-        _check(st)
-        verts = np.zeros(0, dtype=np.int32)
+    st = lib.cc_fetch_cycles(r.handle, first, max_cycles, _ptr(verts), verts.size, _ptr(offsets),
+                             ctypes.byref(nf))
+    if st == 8:  # BUFFER_TOO_SMALL (max_len underestimated): offsets tell the size
+        verts = np.empty(max(int(offsets[k]), 1), dtype=np.int32)
+        st = lib.cc_fetch_cycles(r.handle, first, max_cycles, _ptr(verts), verts.size, _ptr(offsets),
+                                 ctypes.byref(nf))
+    _check(st)
     k = int(nf.value)
+    if k == 0:
+        offsets[0] = 0
     return verts[:int(offsets[k])], offsets[:k + 1]
 
 

@@ -1049,13 +1049,16 @@ extern "C" cc_status cc_fetch_cycles(const cc_result *r, uint64_t first, uint64_
         }
     } restore{cur};
     cudaStream_t st = nullptr;
+    // scratch from the stream-ordered pool (reused across batches, no device-wide sync)
     uint32_t *d_len = nullptr;
-    CC_CUDA(cudaMalloc(&d_len, cnt * 4));
+    CC_CUDA(cudaMallocAsync(&d_len, cnt * 4, st));
     std::vector<uint32_t> len(cnt);
     cudaError_t e = cc::launch_cycle_lengths(r->cyc, r->nw, first, cnt, d_len, st);
     if (e == cudaSuccess)
-        e = cudaMemcpy(len.data(), d_len, cnt * 4, cudaMemcpyDeviceToHost);
-    cudaFree(d_len);
+        e = cudaMemcpyAsync(len.data(), d_len, cnt * 4, cudaMemcpyDeviceToHost, st);
+    cudaFreeAsync(d_len, st);
+    if (e == cudaSuccess)
+        e = cudaStreamSynchronize(st);
     if (e != cudaSuccess)
         return cuda_fail(e, "cycle lengths");
     offsets[0] = 0;
@@ -1066,16 +1069,18 @@ extern "C" cc_status cc_fetch_cycles(const cc_result *r, uint64_t first, uint64_
         return fail(CC_ERR_BUFFER_TOO_SMALL, "vertices needs " + std::to_string(total) + " entries");
     u64 *d_off = nullptr;
     int32_t *d_v = nullptr;
-    CC_CUDA(cudaMalloc(&d_off, (cnt + 1) * 8));
-    e = cudaMalloc(&d_v, std::max<u64>(total, 1) * 4);
+    CC_CUDA(cudaMallocAsync(&d_off, (cnt + 1) * 8, st));
+    e = cudaMallocAsync(&d_v, std::max<u64>(total, 1) * 4, st);
     if (e == cudaSuccess)
-        e = cudaMemcpy(d_off, offsets, (cnt + 1) * 8, cudaMemcpyHostToDevice);
+        e = cudaMemcpyAsync(d_off, offsets, (cnt + 1) * 8, cudaMemcpyHostToDevice, st);
     if (e == cudaSuccess)
         e = cc::launch_cycle_sequences(r->cyc, r->nw, r->adj, r->orig, first, cnt, d_off, d_v, st);
     if (e == cudaSuccess)
-        e = cudaMemcpy(vertices, d_v, total * 4, cudaMemcpyDeviceToHost);
-    cudaFree(d_off);
-    cudaFree(d_v);
+        e = cudaMemcpyAsync(vertices, d_v, total * 4, cudaMemcpyDeviceToHost, st);
+    cudaFreeAsync(d_off, st);
+    cudaFreeAsync(d_v, st);
+    if (e == cudaSuccess)
+        e = cudaStreamSynchronize(st);
     if (e != cudaSuccess)
         return cuda_fail(e, "cycle sequences");
     *n_fetched = cnt;
