@@ -781,6 +781,10 @@ static cc_status enumerate_impl(const cc_graph *cg, const cc_options *opt_in, cc
     levels[3].init = true;
     levels[3].sharded = W == 1 || s1_filter;
     int deepest = 2;  // levels 3..deepest may be non-empty
+    // small-frontier fast path (cc::SmallArgs): count mode, bitset records, n <= 128, one shard
+    const bool small_ok = mode == cc::Mode::B && !wide && !list && nw <= 2 && W == 1 &&
+                          std::getenv("CC_NO_SMALL") == nullptr;
+    bool small_tried = false;
     std::vector<uint32_t> used;
 
     while (true) {
@@ -814,6 +818,87 @@ static cc_status enumerate_impl(const cc_graph *cg, const cc_options *opt_in, cc
         }
         const int d = deepest;
         Level &L = levels[d];
+        // ---- small frontiers: the first levels in one cooperative launch (no host round trip
+        //      per level); the level where the frontier grows past a page is handed back here
+        if (small_ok && !small_tried && d == 3 && s1_next >= stage1_total && L.pages.size() == 1 &&
+            !free_pages.empty() && L.count <= P / (u64)std::max<int64_t>(1, g->max_deg - 1)) {
+            small_tried = true;
+            const size_t na = (size_t)n + 3;
+            DevBuf sm;
+            sm.st = st;
+            CC_CUDA(cudaMallocAsync(&sm.p, (3 * na + 3) * 8, st));
+            CC_CUDA(cudaMemsetAsync(sm.p, 0, (3 * na + 3) * 8, st));
+            u64 *d_count = (u64 *)sm.p, *d_cyc = d_count + na, *d_cand = d_cyc + na, *d_misc = d_cand + na;
+            const u64 c3 = L.count;
+            CC_CUDA(cudaMemcpyAsync(d_count + 3, &c3, 8, cudaMemcpyHostToDevice, st));
+            const uint32_t pg0 = free_pages.back();
+            free_pages.pop_back();
+            cc::SmallArgs sa{};
+            sa.page[0] = pg0;
+            sa.page[1] = L.pages[0];
+            sa.d0 = 3;
+            sa.d_stop = max_len == 0 ? (int)n + 2 : (int)max_len - 2;  // leaf levels stay paged
+            sa.max_len = max_len;
+            sa.threshold = P / (u64)std::max<int64_t>(1, g->max_deg - 1);  // children fit a page
+            sa.count = d_count;
+            sa.cyc = d_cyc;
+            sa.cand = d_cand;
+            sa.hash = d_misc;
+            sa.last = (int32_t *)(d_misc + 1);
+            sa.err = d_misc + 2;
+            cc::LaunchArgs a = base;
+            if (opt.profile)
+                CC_CUDA(cudaEventRecord(ea, st));
+            CC_CUDA(cc::launch_small(a, sa, st, sms));
+            if (opt.profile)
+                CC_CUDA(cudaEventRecord(eb, st));
+            std::vector<u64> h(3 * na + 3);
+            CC_CUDA(cudaMemcpyAsync(h.data(), sm.p, h.size() * 8, cudaMemcpyDeviceToHost, st));
+            CC_CUDA(cudaStreamSynchronize(st));
+            S.d2h_bytes += h.size() * 8;
+            S.launches++;
+            S.chunks++;
+            if (opt.profile) {
+                float ms = 0;
+                CC_CUDA(cudaEventElapsedTime(&ms, ea, eb));
+                S.t_expand_ms += ms;
+            }
+            const u64 *hc = h.data(), *hy = hc + na, *hd = hy + na, *hm = hd + na;  // count, cyc, cand, misc
+            const int last = (int)(int32_t)(hm[1] & 0xffffffffu);
+            if (hm[2])
+                return fail(CC_ERR_CAPACITY, "small-frontier path overflowed a page (internal sizing error)");
+            if (last < 3 || last > (int)n + 2)
+                return fail(CC_ERR_CUDA, "small-frontier path returned a bad level");
+            res->hash += hm[0];
+            for (int t = 3; t < last; ++t) {  // the levels expanded in the cooperative launch
+                res->paths[t] += hc[t];
+                res->cand[t] += hd[t];
+                res->counts[t + 1] += hy[t];
+                S.paths_expanded += hc[t];
+                S.bytes_alg += (hc[t] + hc[t + 1]) * rec_bytes;
+                S.paths_written += hc[t + 1];
+                S.rounds = std::max<u64>(S.rounds, (u64)t);
+            }
+            // the level `last` (possibly empty) continues on the paged path
+            const uint32_t keep = last & 1 ? L.pages[0] : pg0, drop = last & 1 ? pg0 : L.pages[0];
+            free_pages.push_back(drop);
+            in_use -= L.count;
+            L.pages.clear();
+            L.count = 0;
+            Level &N = levels[last];
+            N.pages.assign(1, keep);
+            N.count = hc[last];
+            N.init = true;
+            N.sharded = true;
+            in_use += N.count;
+            high_water = std::max(high_water, in_use);
+            if (N.count == 0) {
+                free_pages.push_back(keep);
+                N.pages.clear();
+            }
+            deepest = last;
+            continue;
+        }
         // ---- multi-GPU: partition the first frontier level with >= threshold paths
         if (W > 1 && !L.sharded && (L.count >= shard_threshold || L.shard_now)) {
             bool of = false;

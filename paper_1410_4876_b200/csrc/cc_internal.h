@@ -137,6 +137,24 @@ cudaError_t launch_expand(const LaunchArgs &a, Mode m, ExpandVariant v, cudaStre
 cudaError_t launch_shard_filter(const LaunchArgs &a, Mode m, cudaStream_t st, int grid_cap);
 cudaError_t launch_keys(u64 *key, u64 *keybyte, const int32_t *orig, int n, int nw, u64 seed,
                         cudaStream_t st);
+// Small-frontier fast path (count mode, bitset records, n <= 128, one shard): all Stage-2
+// levels whose frontier stays small run in ONE cooperative launch with a grid-wide barrier
+// between levels, ping-ponging between two arena pages; it stops (hands the current level to
+// the paged scheduler) when a level could outgrow a page or reaches the last (leaf) level.
+struct SmallArgs {
+    uint32_t page[2];            // the two arena pages (level d lives in page[d & 1])
+    int32_t d0;                  // first level (3: the triplets, in page[1])
+    int32_t d_stop;              // levels d0 .. d_stop-1 may run here (leaf levels excluded)
+    uint32_t max_len;            // cc_options.max_len
+    u64 threshold;               // a level with more input paths is handed off
+    u64 *count;                  // [n+3] count[d] = |F_d| written (count[d0] set by the host)
+    u64 *cyc;                    // [n+3] closures of length d+1 found at level d
+    u64 *cand;                   // [n+3] candidate slots of level d
+    u64 *hash;                   // sum of h(C)
+    int32_t *last;               // the level the kernel stopped at (its records are in page[last & 1])
+    u64 *err;                    // overflow (must stay 0: the threshold guarantees room)
+};
+cudaError_t launch_small(const LaunchArgs &a, const SmallArgs &s, cudaStream_t st, int sms);
 // nbrmask (DevGraph) of a wide graph with Delta <= 32; T must be zeroed, n*n words
 cudaError_t launch_nbrmask(const DevGraph &g, uint32_t *T, cudaStream_t st);
 cudaError_t launch_cycle_lengths(const CycleStore &c, int nw, uint64_t first, uint64_t count,

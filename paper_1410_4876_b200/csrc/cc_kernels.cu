@@ -31,6 +31,8 @@
 //   extend iff X == {}, close iff X == {v1}.
 #include "cc_internal.h"
 
+#include <cooperative_groups.h>
+
 namespace cc {
 
 #define FULL_MASK 0xffffffffu
@@ -1107,6 +1109,171 @@ __global__ void __launch_bounds__(kBlock) k_expand_warp(const LaunchArgs p)
     if (!p.count)
         cand = 0;
     flush_accum(cnt, hs, cand, p.sc);
+}
+
+// ---------------------------------------------------------------------------- small frontiers
+// k_small_levels (SmallArgs): the Stage-2 levels of a small frontier in one cooperative launch.
+// Thread per path on the blocked-vertex record (the test of k_expand_blocked, closed rows),
+// children appended with one atomic per CTA iteration; a grid-wide barrier separates levels, so
+// a level costs a barrier instead of a host round trip (launch + scratch read-back + sync).
+template <int NW, bool PACK>
+__global__ void __launch_bounds__(kBlock) k_small_levels(const LaunchArgs p, const SmallArgs s)
+{
+    namespace cg = cooperative_groups;
+    constexpr int RW = NW + 1;
+    extern __shared__ __align__(16) u64 smem[];
+    u64 *s_adj = smem;                   // closed rows
+    u64 *s_key = s_adj + p.g.n * NW;
+    u64 *s_above = s_key + ((p.g.n + 1) & ~1);
+    __shared__ ReserveSmem rs;
+    for (int i = threadIdx.x; i < p.g.n * NW; i += kBlock) {
+        s_above[i] = above_word((uint32_t)(i / NW), i % NW);
+        s_adj[i] = p.g.adj[i] | bit_in_word(i % NW, (uint32_t)(i / NW));
+    }
+    for (int i = threadIdx.x; i < p.g.n; i += kBlock)
+        s_key[i] = p.g.key[i];
+    __syncthreads();
+    cg::grid_group grid = cg::this_grid();
+    const uint32_t idb = PACK ? p.idb : (uint32_t)kIdBits;
+    const uint32_t idm = (1u << idb) - 1;
+    const u64 keep_v12 = PACK ? ~((u64)idm << (64 - idb)) : ~0ull;
+    const u64 P = 1ull << p.pg.log_p;
+    int d = s.d0;
+    for (;;) {
+        const u64 n_in = s.count[d];
+        if (n_in == 0 || d >= s.d_stop || n_in > s.threshold)
+            break;  // block-uniform: everybody read the same count after the barrier
+        const char *ip = p.pg.base + (u64)s.page[d & 1] * p.pg.page_bytes;
+        char *op = p.pg.base + (u64)s.page[(d + 1) & 1] * p.pg.page_bytes;
+        const bool emit = s.max_len == 0 || (u64)d + 1 < s.max_len;
+        uint32_t cnt = 0, cand = 0;
+        u64 hs = 0;
+        const u64 stride = (u64)gridDim.x * kBlock;
+        for (u64 base = (u64)blockIdx.x * kBlock; base < n_in; base += stride) {
+            const u64 r = base + threadIdx.x;
+            u64 W[RW], ext[NW];
+            uint32_t id = 0, ne = 0;
+#pragma unroll
+            for (int w = 0; w < NW; ++w)
+                ext[w] = 0;
+            if (r < n_in) {
+#pragma unroll
+                for (int w = 0; w < RW; ++w)
+                    W[w] = ((const u64 *)ip)[(u64)w * P + r];
+                id = PACK ? (uint32_t)packed_ids(W[NW - 1], idb) : ((const uint32_t *)(ip + (u64)RW * P * 8))[r];
+                const uint32_t v1 = id & idm, v2 = (id >> idb) & idm, vt = id >> (2 * idb);
+                u64 arow[NW], abv[NW], a1[NW];
+                lds_row<NW>(s_adj, vt, arow);
+                lds_row<NW>(s_above, v2, abv);
+                lds_row<NW>(s_adj, v1, a1);
+                cand -= 1;  // closed row
+#pragma unroll
+                for (int w = 0; w < NW; ++w) {
+                    cand += __popcll(arow[w]);
+                    const u64 c = arow[w] & abv[w] & ~W[w];
+                    u64 cl = c & a1[w];
+                    ext[w] = emit ? (c & ~a1[w]) : 0ull;
+                    ne += __popcll(ext[w]);
+                    cnt += __popcll(cl);
+                    while (cl) {
+                        const int b = __ffsll((long long)cl) - 1;
+                        cl &= cl - 1;
+                        hs += mix64(W[NW] + s_key[64 * w + b]);
+                    }
+                }
+            }
+            const u64 off = block_reserve(ne, &s.count[d + 1], rs);
+            if (ne) {
+                if (off + ne > P) {
+                    *s.err = 1;
+                } else {
+                    const uint32_t vt = id >> (2 * idb), v12 = id & ((1u << (2 * idb)) - 1);
+                    u64 C[RW];
+#pragma unroll
+                    for (int w = 0; w < NW; ++w)
+                        C[w] = W[w] | s_adj[vt * NW + w];  // B | N[vt]
+                    C[NW - 1] &= keep_v12;
+                    u64 o = off;
+#pragma unroll
+                    for (int w = 0; w < NW; ++w) {
+                        u64 m = ext[w];
+                        while (m) {
+                            const int b = __ffsll((long long)m) - 1;
+                            m &= m - 1;
+                            const uint32_t v = (uint32_t)(64 * w + b);
+                            u64 X[RW];
+#pragma unroll
+                            for (int q = 0; q < RW; ++q)
+                                X[q] = C[q];
+                            X[NW] = W[NW] + s_key[v];
+                            if (PACK)
+                                X[NW - 1] |= (u64)v << (64 - idb);
+                            else
+                                ((uint32_t *)(op + (u64)RW * P * 8))[o] = v12 | (v << (2 * idb));
+#pragma unroll
+                            for (int q = 0; q < RW; ++q)
+                                ((u64 *)op)[(u64)q * P + o] = X[q];
+                            ++o;
+                        }
+                    }
+                }
+            }
+        }
+        // level statistics: one atomic per counter per CTA
+        Acc a;
+        a.cyc = cnt;
+        a.cand = cand;
+        a.hash = hs;
+        {
+            constexpr int K = 3;
+            __shared__ u64 red[K][kBlock / 32];
+            u64 v[K] = {a.cyc, a.cand, a.hash};
+            const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+#pragma unroll
+            for (int k = 0; k < K; ++k) {
+#pragma unroll
+                for (int o = 16; o > 0; o >>= 1)
+                    v[k] += __shfl_xor_sync(FULL_MASK, v[k], o);
+                if (lane == 0)
+                    red[k][wid] = v[k];
+            }
+            __syncthreads();
+            if (threadIdx.x < K) {
+                u64 t = 0;
+                for (int i = 0; i < kBlock / 32; ++i)
+                    t += red[threadIdx.x][i];
+                u64 *dst = threadIdx.x == 0 ? &s.cyc[d] : threadIdx.x == 1 ? &s.cand[d] : s.hash;
+                if (t)
+                    atomicAdd(dst, t);
+            }
+        }
+        grid.sync();
+        ++d;
+    }
+    if (blockIdx.x == 0 && threadIdx.x == 0)
+        *s.last = d;
+}
+
+cudaError_t launch_small(const LaunchArgs &a, const SmallArgs &s, cudaStream_t st, int sms)
+{
+    void (*f)(const LaunchArgs, const SmallArgs) = nullptr;
+    if (a.g.nw == 1)
+        f = a.packed ? k_small_levels<1, true> : k_small_levels<1, false>;
+    else if (a.g.nw == 2)
+        f = a.packed ? k_small_levels<2, true> : k_small_levels<2, false>;
+    if (!f)
+        return cudaErrorInvalidValue;
+    const size_t smem = ((size_t)a.g.n * 2 * a.g.nw + ((a.g.n + 1) & ~1)) * sizeof(u64);
+    int nb = 0;
+    cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, (const void *)f, kBlock, smem);
+    if (e != cudaSuccess)
+        return e;
+    if (nb < 1)
+        return cudaErrorInvalidConfiguration;
+    LaunchArgs a2 = a;
+    SmallArgs s2 = s;
+    void *args[] = {(void *)&a2, (void *)&s2};
+    return cudaLaunchCooperativeKernel((const void *)f, dim3((unsigned)(nb * sms)), dim3(kBlock), args, smem, st);
 }
 
 // ---------------------------------------------------------------------------- shard filter
