@@ -441,3 +441,23 @@ def test_full_size_against_oracle_golden(ws, name):
     assert f"{got['set_hash']:#018x}" == want["set_hash"]
     assert {str(k): int(v) for k, v in enumerate(got["paths_by_len"]) if v} == want["paths_by_len"]
     assert got["candidates"] == want["candidates"]
+
+
+@pytest.mark.parametrize("name,g,K", [("grid5x6", I.grid(5, 6), 0), ("grid6x10", I.grid(6, 10), 0),
+                                      ("k8x8", I.complete_bipartite(8, 8), 0), ("grid7x10_k14", I.grid(7, 10), 14),
+                                      ("gnp90", I.gnp(90, 0.08, 5), 9), ("p4x4", I.grid(4, 4), 0)])
+def test_small_frontier_path(ws, name, g, K):
+    """The small-frontier fast path (one cooperative launch for the first levels)
+    gives the oracle's counts, hash, |F_t| and candidates, and so does the paged path alone
+    (CC_NO_SMALL); on the small grids it replaces the per-level launches."""
+    want = oracle.enumerate_cycles(*g, max_len=K, nthreads=NT)
+    got = gpu(g, ws, max_len=K)
+    assert_same(got, want)
+    os.environ["CC_NO_SMALL"] = "1"
+    try:
+        paged = gpu(g, ws, max_len=K)
+    finally:
+        del os.environ["CC_NO_SMALL"]
+    assert_same(paged, want)
+    if name in ("grid5x6", "p4x4"):
+        assert got["stats"]["launches"] == 2 < paged["stats"]["launches"]
