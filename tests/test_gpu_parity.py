@@ -461,3 +461,20 @@ def test_small_frontier_path(ws, name, g, K):
     assert_same(paged, want)
     if name in ("grid5x6", "p4x4"):
         assert got["stats"]["launches"] == 2 < paged["stats"]["launches"]
+
+
+@pytest.mark.parametrize("name,g,K", [
+    ("star600", I.star(600), 6),                 # wide class, Delta = 600: bitset only, no cycles
+    ("cycle700", I.cycle(700), 0),               # wide class, one chordless cycle of 700 vertices
+    ("complete40", I.complete(40), 0),           # triangles only: C(40, 3)
+    ("gnp2015_list", I.gnp(2015, 0.0018, 77), 14),  # the largest n, the longest list records
+    ("grid30x30_isolated", I.edges_to_csr(1000, [(a, b) for a, b in zip(*np.nonzero(np.triu(np.eye(900, k=1) + np.eye(900, k=30))))
+                                                 if (b == a + 30) or (a % 30 != 29)]), 8),  # 100 isolated vertices
+])
+def test_degenerate_and_extreme_graphs(ws, name, g, K):
+    got = gpu(g, ws, max_len=K)
+    assert_same(got, oracle.enumerate_cycles(*g, max_len=K, nthreads=NT))
+    if name == "cycle700":
+        assert int(got["counts"][700]) == 1 and int(got["counts"].sum()) == 1
+    if name == "complete40":
+        assert int(got["counts"][3]) == math.comb(40, 3) and int(got["counts"].sum()) == math.comb(40, 3)
