@@ -18,7 +18,10 @@ constexpr uint32_t kIdMask = (1u << kIdBits) - 1;
 #endif
 constexpr int kBlock = CC_BLOCK;       // threads per CTA for every kernel
 // R: paths per thread per tile in k_expand_thread
-__host__ __device__ constexpr int expand_paths_per_thread(int nw) { return nw <= 4 ? 2 : 1; }
+#ifndef CC_EB_R
+#define CC_EB_R 2
+#endif
+__host__ __device__ constexpr int expand_paths_per_thread(int nw) { return nw <= 4 ? CC_EB_R : 1; }
 constexpr int kMinLogPage = 10;        // pages hold >= kBlock * R records (one CTA tile)
 constexpr int kByteTableWords = 2;     // byte-wise key tables (H-spec keysum) for NW <= 2
 

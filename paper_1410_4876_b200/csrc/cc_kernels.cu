@@ -1121,7 +1121,7 @@ __global__ void __launch_bounds__(kBlock) k_small_levels(const LaunchArgs p, con
 {
     namespace cg = cooperative_groups;
     constexpr int RW = NW + 1;
-    extern __shared__ __align__(16) u64 smem[];
+    extern __shared__ __align__(128) u64 smem[];
     u64 *s_adj = smem;                   // closed rows
     u64 *s_key = s_adj + p.g.n * NW;
     u64 *s_above = s_key + ((p.g.n + 1) & ~1);
