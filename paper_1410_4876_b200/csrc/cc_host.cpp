@@ -193,15 +193,26 @@ extern "C" cc_status cc_graph_from_csr(int64_t n, const int64_t *row_ptr, const 
                 return fail(CC_ERR_SELF_LOOP, "self-loop at vertex " + std::to_string(v));
             cl.push_back(w);
         }
-        std::sort(cl.begin() + b, cl.end());
+        if (!std::is_sorted(cl.begin() + b, cl.end()))
+            std::sort(cl.begin() + b, cl.end());
         cl.erase(std::unique(cl.begin() + b, cl.end()), cl.end());
         rp[v + 1] = (int64_t)cl.size();
     }
-    // symmetry: w in row v  <=>  v in row w
+    // symmetry: w in row v  <=>  v in row w.  Small graphs (every size class that runs, n <=
+    // 2015): an n x n bit matrix, O(n^2/64 + m); larger ones: binary search per entry
+    const bool small_n = n <= 4096;
+    const int64_t mw = (n + 63) / 64;
+    std::vector<u64> M(small_n ? (size_t)n * mw : 0, 0);
+    if (small_n)
+        for (int64_t v = 0; v < n; ++v)
+            for (int64_t k = rp[v]; k < rp[v + 1]; ++k)
+                M[(size_t)v * mw + (cl[k] >> 6)] |= 1ull << (cl[k] & 63);
     for (int64_t v = 0; v < n; ++v)
         for (int64_t k = rp[v]; k < rp[v + 1]; ++k) {
             const int32_t w = cl[k];
-            if (!std::binary_search(cl.begin() + rp[w], cl.begin() + rp[w + 1], (int32_t)v))
+            const bool rev = small_n ? ((M[(size_t)w * mw + (v >> 6)] >> (v & 63)) & 1ull) != 0
+                                     : std::binary_search(cl.begin() + rp[w], cl.begin() + rp[w + 1], (int32_t)v);
+            if (!rev)
                 return fail(CC_ERR_NOT_SYMMETRIC, "edge (" + std::to_string(v) + "," +
                                                       std::to_string(w) + ") has no reverse entry");
         }
@@ -220,13 +231,34 @@ extern "C" cc_status cc_graph_from_csr(int64_t n, const int64_t *row_ptr, const 
     g->icol.resize(cl.size());
     g->ifwd.assign(n, 0);
     g->pair_prefix.assign(n + 1, 0);
+    // rows in label space: small graphs scatter the relabelled edges into a label-space bit
+    // matrix and read each row back in order (no per-row sort)
+    std::vector<u64> LM(small_n ? (size_t)n * mw : 0, 0);
+    if (small_n)
+        for (int64_t v = 0; v < n; ++v) {
+            const int64_t lv = g->label[v];
+            for (int64_t e = rp[v]; e < rp[v + 1]; ++e) {
+                const int32_t lw = g->label[cl[e]];
+                LM[(size_t)lv * mw + (lw >> 6)] |= 1ull << (lw & 63);
+            }
+        }
     for (int64_t i = 0; i < n; ++i) {
         const int32_t v = g->perm[i];
         const uint32_t b = g->irow[i];
         uint32_t k = b;
-        for (int64_t e = rp[v]; e < rp[v + 1]; ++e)
-            g->icol[k++] = (uint32_t)g->label[cl[e]];
-        std::sort(g->icol.begin() + b, g->icol.begin() + k);
+        if (small_n) {
+            for (int64_t w = 0; w < mw; ++w) {
+                u64 x = LM[(size_t)i * mw + w];
+                while (x) {
+                    g->icol[k++] = (uint32_t)(64 * w + __builtin_ctzll(x));
+                    x &= x - 1;
+                }
+            }
+        } else {
+            for (int64_t e = rp[v]; e < rp[v + 1]; ++e)
+                g->icol[k++] = (uint32_t)g->label[cl[e]];
+            std::sort(g->icol.begin() + b, g->icol.begin() + k);
+        }
         g->irow[i + 1] = k;
         uint32_t f = b;
         while (f < k && g->icol[f] <= (uint32_t)i)
@@ -246,11 +278,17 @@ extern "C" cc_status cc_graph_from_csr(int64_t n, const int64_t *row_ptr, const 
         g->nw = wide_nw ? wide_nw : (n > 0 ? (int)((n + 63) / 64) : 1);
         g->wide = wide_nw != 0;
         g->adj.assign((size_t)n * g->nw, 0);
-        for (int64_t i = 0; i < n; ++i)
-            for (uint32_t k = g->irow[i]; k < g->irow[i + 1]; ++k) {
-                const uint32_t w = g->icol[k];
-                g->adj[(size_t)i * g->nw + (w >> 6)] |= 1ull << (w & 63);
-            }
+        if (small_n && g->nw >= mw) {
+            for (int64_t i = 0; i < n; ++i)
+                std::copy(LM.begin() + (size_t)i * mw, LM.begin() + (size_t)(i + 1) * mw,
+                          g->adj.begin() + (size_t)i * g->nw);
+        } else {
+            for (int64_t i = 0; i < n; ++i)
+                for (uint32_t k = g->irow[i]; k < g->irow[i + 1]; ++k) {
+                    const uint32_t w = g->icol[k];
+                    g->adj[(size_t)i * g->nw + (w >> 6)] |= 1ull << (w & 63);
+                }
+        }
     }
     g->t_build_ms = now_ms() - t0;
     *out = g;
