@@ -128,6 +128,47 @@ extern "C" const char *cc_version(void) { return "chordless-b200 0.1 (sm_100a)";
 static void degree_labeling(int64_t n, const std::vector<int64_t> &rp, const std::vector<int32_t> &cl,
                             std::vector<int32_t> &label)
 {
+    if (n > 0 && n <= 4096) {
+        // small graphs: one n-bit set per degree; the next vertex is the lowest set bit of the
+        // lowest non-empty degree (ties -> lowest id), O(n^2/64 + m) in all
+        const int64_t words = (n + 63) / 64;
+        int64_t maxd = 0;
+        std::vector<int64_t> d(n);
+        for (int64_t v = 0; v < n; ++v) {
+            d[v] = rp[v + 1] - rp[v];
+            maxd = std::max(maxd, d[v]);
+        }
+        std::vector<u64> bucket((size_t)(maxd + 1) * words, 0);
+        for (int64_t v = 0; v < n; ++v)
+            bucket[(size_t)d[v] * words + (v >> 6)] |= 1ull << (v & 63);
+        label.assign(n, -1);
+        int64_t cur = 0;
+        for (int64_t i = 0; i < n; ++i) {
+            int32_t u = -1;
+            while (u < 0) {
+                const u64 *b = &bucket[(size_t)cur * words];
+                for (int64_t w = 0; w < words; ++w)
+                    if (b[w]) {
+                        u = (int32_t)(64 * w + __builtin_ctzll(b[w]));
+                        break;
+                    }
+                if (u < 0)
+                    ++cur;
+            }
+            bucket[(size_t)d[u] * words + (u >> 6)] &= ~(1ull << (u & 63));
+            label[u] = (int32_t)i;
+            for (int64_t k = rp[u]; k < rp[u + 1]; ++k) {
+                const int32_t w = cl[k];
+                if (label[w] < 0) {
+                    bucket[(size_t)d[w] * words + (w >> 6)] &= ~(1ull << (w & 63));
+                    --d[w];
+                    bucket[(size_t)d[w] * words + (w >> 6)] |= 1ull << (w & 63);
+                    cur = std::min(cur, d[w]);
+                }
+            }
+        }
+        return;
+    }
     typedef std::pair<int64_t, int32_t> Key;
     std::vector<int64_t> d(n);
     std::vector<Key> heap;
