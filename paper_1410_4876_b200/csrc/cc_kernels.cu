@@ -536,6 +536,9 @@ __global__ void __launch_bounds__(kBlock) k_stage1(const LaunchArgs p)
 #define CC_CHILD_CAP_X4 8
 #endif
 constexpr int kStages = CC_STAGES;
+#ifndef CC_STORE_CS
+#define CC_STORE_CS 0  // 1 = cache-streaming stores for the children (st.global.cs)
+#endif
 #ifndef CC_EB_BLOCK
 #define CC_EB_BLOCK 128
 #endif
@@ -885,8 +888,13 @@ __global__ void __launch_bounds__(kEBBlock, NW <= 2 ? CC_EB_MINB : 2) k_expand_b
                     ((uint32_t *)(pp + ((u64)RW << p.pg.log_p) * 8))[oslot] = s_pid[slot] | (v << (2 * idb));
                 }
 #pragma unroll
-                for (int w = 0; w < RW; ++w)
+                for (int w = 0; w < RW; ++w) {
+#if CC_STORE_CS
+                    __stcs(w0 + ((size_t)w << p.pg.log_p), C[w]);  // streaming: evict-first in L2
+#else
                     w0[(size_t)w << p.pg.log_p] = C[w];
+#endif
+                }
             }
         }
     }
