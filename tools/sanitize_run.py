@@ -23,6 +23,13 @@ cases = [
     ("gnp600 count (wide class)", I.gnp(600, 0.01, 5), dict(max_len=8)),
     ("gnp600 count shard 0/2 (wide filter)", I.gnp(600, 0.01, 5), dict(max_len=7, shard_index=0, shard_count=2,
                                                                         min_shard_paths=16)),
+    ("p5x6 count (small-frontier cooperative kernel)", I.grid(5, 6), {}),
+    ("p6x7 count K=12 (blocked LEAF variant)", I.grid(6, 7), dict(max_len=12)),
+    ("gnp600 count K=7 (wide bitset + k_leaf_wide)", I.gnp(600, 0.01, 5), dict(max_len=7, record_format=1)),
+    ("gnp700 count K=8 (list class + list leaf)", I.gnp(700, 0.008, 11), dict(max_len=8, record_format=2)),
+    ("grid24x24 count K=13 (list class, 3 id words)", I.grid(24, 24), dict(max_len=13, record_format=2)),
+    ("gnp700 count K=8 shard 1/2 (list filter)", I.gnp(700, 0.008, 11), dict(max_len=8, record_format=2, shard_index=1,
+                                                                            shard_count=2, min_shard_paths=16)),
 ]
 bad = 0
 for name, g, kw in cases:
