@@ -157,6 +157,22 @@ def oracle_sample(workload: str, g):
     return int(r["counts"].sum()), int(r["paths_by_len"].sum()), dt, cores, desc
 
 
+def oracle_full_config(workload: str):
+    """The oracle on the WHOLE workload, as recorded in its golden file (tests/golden/, written by
+    tests/golden/make_oracle_big.py on the GPU box's host cores): too slow to rerun per bench."""
+    name = {"gnp2000": "gnp2000_k9", "gnp2000k10": "gnp2000_k10"}.get(workload, workload)
+    path = os.path.join(ROOT, "tests", "golden", f"oracle_{name}.json")
+    if not os.path.exists(path):
+        return None
+    d = json.load(open(path))
+    sec = d.get("oracle_seconds")
+    if not sec:
+        return None
+    return {"value": d["total"] / sec, "unit": UNIT, "paths_per_s": d["paths_total"] / sec,
+            "seconds": sec, "cores": d.get("oracle_threads"), "host": d.get("host"),
+            "source": f"tests/golden/oracle_{name}.json"}
+
+
 def run_reference(args, workload, g):
     rank, world, _ = dist_env()
     if rank != 0:
@@ -183,6 +199,43 @@ def run_reference(args, workload, g):
     return 0
 
 
+def _free_port() -> int:
+    import socket
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        return sk.getsockname()[1]
+
+
+def launch_ranks(args) -> int | None:
+    """--gpus N: one process per GPU.  Under torchrun (WORLD_SIZE set) the world must equal N;
+    without it, N > 1 re-executes this script under torch.distributed.run with N ranks on
+    127.0.0.1 (so `python bench.py --gpus 8` measures 8 ranks, never silently one).  Returns
+    None to continue in this process, else the exit code to return."""
+    if "WORLD_SIZE" in os.environ:
+        world = int(os.environ["WORLD_SIZE"])
+        if world != args.gpus:
+            print(f"error: WORLD_SIZE={world} but --gpus {args.gpus}: launch one rank per GPU",
+                  file=sys.stderr)
+            return 2
+        return None
+    if args.gpus <= 1:
+        return None
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr", "127.0.0.1", "--master-port", str(_free_port()), os.path.abspath(__file__),
+           *sys.argv[1:]]
+    return subprocess.call(cmd)
+
+
+def r_alg_bytes(n: int, record_format: int) -> int:
+    """SURVEY §8(d) minimal algorithmic record: ceil(n/8) bytes of the path set S
+    plus three ids v1, v2, vt of ceil(log2(n)/8) bytes each -- 11 B at n = 64,
+    16 B at n = 100, 44 B at n = 300; the list class (n = 2000, t <= 10) is 20 B."""
+    if record_format == 2:
+        return 20
+    idb = 1 if n <= 256 else 2
+    return (n + 7) // 8 + 3 * idb
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -198,6 +251,10 @@ def main():
     if args.warmup < 3 and args.impl == "ours":
         print("warning: the contract asks for >= 3 warm-up steps", file=sys.stderr)
 
+    rc = launch_ranks(args)
+    if rc is not None:
+        return rc
+
     build_fn, max_len, wdesc = WORKLOADS[args.workload]
     g = build_fn()
     if args.impl == "reference":
@@ -209,10 +266,13 @@ def main():
     from paper_1410_4876_b200 import binding
 
     rank, world, local = dist_env()
-    # one process per GPU; CC_DIST_BACKEND=gloo (+ several ranks per GPU) is only for checking
-    # the N > 1 path on a one-GPU box
-    backend = os.environ.get("CC_DIST_BACKEND", "nccl")
-    local = local % max(torch.cuda.device_count(), 1)
+    # one process per GPU over NCCL.  More ranks than GPUs (only to exercise the N > 1 path on a
+    # one-GPU box) share devices, which NCCL refuses: those runs use gloo for the two small
+    # reductions (CC_DIST_BACKEND overrides)
+    ndev = max(torch.cuda.device_count(), 1)
+    ranks_per_dev = (world + ndev - 1) // ndev
+    backend = os.environ.get("CC_DIST_BACKEND", "nccl" if ranks_per_dev == 1 else "gloo")
+    local = local % ndev
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     if world > 1:
@@ -224,9 +284,17 @@ def main():
     stream = torch.cuda.current_stream()
     sh = stream.cuda_stream
 
-    free, _ = torch.cuda.mem_get_info()
     l2_flush = torch.empty(512 << 20, dtype=torch.uint8, device=dev)  # > 126 MB L2
-    ws_bytes = int(args.workspace_gb * (1 << 30)) if args.workspace_gb > 0 else int(free * 0.85) - (1 << 30)
+    if world > 1:
+        dist.barrier()  # every rank sharing a device sees the same free memory
+    free, _ = torch.cuda.mem_get_info()
+    ws_bytes = (int(args.workspace_gb * (1 << 30)) if args.workspace_gb > 0
+                else int(free * 0.85 / ranks_per_dev) - (1 << 30))
+    if world > 1:
+        # every rank must use the same arena size (include/chordless.h, min_shard_paths): the
+        # fallback partition of a level that does not fit depends on it
+        from paper_1410_4876_b200 import dist as D
+        ws_bytes = int(D.min_over_ranks(float(ws_bytes), device=dev if backend == "nccl" else None))
     ws = torch.empty(ws_bytes, dtype=torch.uint8, device=dev)
 
     opts = binding.make_options(device=local, stream=sh, max_len=max_len, shard_index=rank,
@@ -258,7 +326,8 @@ def main():
         torch.cuda.synchronize()
     if world > 1:
         dist.barrier()
-    dev_ms = sum(a.elapsed_time(b) for a, b in ev)
+    step_ms = [a.elapsed_time(b) for a, b in ev]
+    dev_ms = sum(step_ms)
     for r in results:
         stats.append(binding.cc_result_stats(r))
     counts, h = binding.cc_count_by_length(results[-1])
@@ -274,38 +343,55 @@ def main():
         per_rank = [{"rank": i, "ms_per_step": v[0] / args.steps, "paths": int(v[1])}
                     for i, v in enumerate(D.gather_per_rank([dev_ms, paths_local], device=comm_dev))]
         dev_ms = D.max_over_ranks(dev_ms, device=comm_dev)
+        step_ms = [D.max_over_ranks(x, device=comm_dev) for x in step_ms]
         counts, h, paths_total = D.combine_shards(counts, h, paths_local, device=comm_dev)
     else:
         paths_total = paths_local
+    cand_total = st_last_cand = stats[-1]["candidates"]
+    if world > 1:
+        cand_total = int(D.combine_shards(np.zeros(1, np.uint64), 0, st_last_cand, device=comm_dev)[2])
     cycles_total = int(counts.sum())
     ms_per_step = dev_ms / args.steps
     value = cycles_total / (ms_per_step / 1e3)
     paths_per_s = paths_total / (ms_per_step / 1e3)
 
-    # ---- roofline of the dominant kernel (Stage-2 expansion), from this rank's live events
+    # ---- roofline of the dominant kernel (Stage-2 expansion), from this rank's live events.
+    # achieved = SURVEY §8(d) algorithmic bytes: R_alg (ceil(n/8) + 3 ids, 16 B at n = 100) per
+    # record read or written by the expansion launches, over their summed CUDA-event time; the
+    # same figure at the record size this build actually stores is reported beside it
     st_last = stats[-1]
     t_expand = sum(s["t_expand_ms"] for s in stats)
-    bytes_alg = sum(s["bytes_alg"] for s in stats)
+    rec_b = st_last["record_bytes"]
+    records_moved = sum(s["bytes_alg"] for s in stats) / rec_b if rec_b else 0.0
+    r_alg = r_alg_bytes(g[0], st_last["record_format"])
+    bytes_alg = records_moved * r_alg
     launches = sum(s["launches"] for s in stats)
     peak, peak_kind = peaks()
     achieved = (bytes_alg / (t_expand / 1e3)) / 1e9 if t_expand > 0 else 0.0
+    achieved_rec = (records_moved * rec_b / (t_expand / 1e3)) / 1e9 if t_expand > 0 else 0.0
     # traffic: dram__bytes_read.sum + dram__bytes_write.sum of one ncu --set full capture of this
-    # kernel (per launch), with the algorithmic bytes of that same launch (from the CC_TRACE log)
-    traffic = traffic_ratio = None
+    # kernel (one launch, profiles/ncu_traffic.json), against that launch's R_alg bytes
+    traffic = traffic_ratio = traffic_src = None
     tp = os.path.join(ROOT, "profiles", "ncu_traffic.json")
     if os.path.exists(tp):
         try:
             t_ = json.load(open(tp)).get(args.workload)
             if t_:
-                traffic, traffic_ratio = t_["dram_bytes"], t_["dram_over_alg"]
+                recs = t_["paths_in"] + t_["children_out"]
+                traffic = t_["dram_bytes"]
+                traffic_ratio = t_["dram_bytes"] / (recs * r_alg)
+                traffic_src = f"profiles/ncu_traffic.json ({t_['kernel']}, {t_['launch']}, {recs} records)"
         except Exception:
-            traffic = traffic_ratio = None
+            traffic = traffic_ratio = traffic_src = None
     roofline = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                 "frac": achieved / peak, "traffic": traffic, "traffic_over_alg": traffic_ratio,
-                "peak_kind": peak_kind,
+                "traffic_source": traffic_src, "peak_kind": peak_kind,
+                "r_alg_bytes": r_alg, "record_bytes": rec_b,
+                "achieved_record_bytes": achieved_rec, "frac_record_bytes": achieved_rec / peak,
                 "kernel": ("k_expand_blocked" if g[0] <= 512 else
                            "k_expand_list" if st_last["record_format"] == 2 else "k_expand_wide"),
                 "expand_share_of_step": t_expand / dev_ms if dev_ms else None,
+                "records_per_step": records_moved / args.steps,
                 "bytes_alg_per_step": bytes_alg / args.steps}
     if st_last["record_format"] == 2:
         # vertex-list records (24 B) move so few bytes that HBM is not the bound: the time goes
@@ -365,6 +451,9 @@ def main():
             c, p, dt, cores, desc = oracle_sample(args.workload, g)
             cpu = {"value": c / dt, "unit": UNIT, "cores": cores, "kind": "oracle", "sample": desc,
                    "paths_per_s": p / dt, "seconds": dt}
+            full = oracle_full_config(args.workload)
+            if full:
+                cpu["full_config"] = full
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True,
@@ -374,6 +463,8 @@ def main():
                        "parallelism": f"shard{world}" if world > 1 else "single",
                        "record_bytes": st_last["record_bytes"], "arena_records": st_last["arena_capacity"]},
             "paths_per_s": paths_per_s, "cycles": cycles_total, "paths_expanded": paths_total,
+            "candidate_slots_per_s": cand_total / (ms_per_step / 1e3),
+            "ms_per_step_median": float(np.median(step_ms)), "ms_per_step_min": float(min(step_ms)),
             "set_hash": f"{h:#018x}", "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e,
             "gpu_launches": launches, "clocks": clk.summary(),
             "frontier_sizes": {str(t): int(v) for t, v in enumerate(paths) if v} if world == 1 else None,

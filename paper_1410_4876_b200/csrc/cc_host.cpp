@@ -375,6 +375,8 @@ extern "C" cc_status cc_graph_labels(const cc_graph *g, int32_t *labels)
 
 static size_t align_up(size_t x, size_t a) { return (x + a - 1) / a * a; }
 
+static cc_status upload_graph(cc_graph *g, int device, cudaStream_t st, DevCopy *dc, uint64_t *h2d);
+
 // Upload (once per device) the relabelled graph; recompute keys when the seed changes.
 static cc_status ensure_device_graph(cc_graph *g, int device, u64 seed, cudaStream_t st, DevCopy **out,
                                      uint64_t *h2d)
@@ -385,8 +387,31 @@ static cc_status ensure_device_graph(cc_graph *g, int device, u64 seed, cudaStre
             dc = &d;
     const int64_t n = g->n;
     if (!dc) {
-        g->dev.emplace_back();
+        // built in a local copy and added to g->dev only when every upload succeeded: a failed
+        // allocation must not leave a half-built entry that a later call would run on
+        DevCopy nd;
+        cc_status s = upload_graph(g, device, st, &nd, h2d);
+        if (s != CC_OK) {
+            if (nd.buf)
+                cudaFree(nd.buf);
+            return s;
+        }
+        g->dev.push_back(nd);
         dc = &g->dev.back();
+    }
+    if (!dc->keys_valid || dc->key_seed != seed) {
+        CC_CUDA(cc::launch_keys((u64 *)dc->dg.key, (u64 *)dc->dg.keybyte, dc->dg.orig, (int)n, g->nw, seed, st));
+        dc->key_seed = seed;
+        dc->keys_valid = true;
+    }
+    *out = dc;
+    return CC_OK;
+}
+
+static cc_status upload_graph(cc_graph *g, int device, cudaStream_t st, DevCopy *dc, uint64_t *h2d)
+{
+    const int64_t n = g->n;
+    {
         dc->device = device;
         const size_t s_row = align_up((n + 1) * 4, 256), s_col = align_up(std::max<size_t>(g->icol.size(), 1) * 4, 256),
                      s_fwd = align_up(std::max<int64_t>(n, 1) * 4, 256), s_pp = align_up((n + 1) * 8, 256),
@@ -435,12 +460,6 @@ static cc_status ensure_device_graph(cc_graph *g, int device, u64 seed, cudaStre
             CC_CUDA(cc::launch_nbrmask(dc->dg, nbrmask, st));
         }
     }
-    if (!dc->keys_valid || dc->key_seed != seed) {
-        CC_CUDA(cc::launch_keys((u64 *)dc->dg.key, (u64 *)dc->dg.keybyte, dc->dg.orig, (int)n, g->nw, seed, st));
-        dc->key_seed = seed;
-        dc->keys_valid = true;
-    }
-    *out = dc;
     return CC_OK;
 }
 
@@ -480,10 +499,15 @@ namespace {
 struct DevBuf {
     void *p = nullptr;
     cudaStream_t st = nullptr;
+    cudaMemPool_t trim_pool = nullptr;  // large blocks: give the memory back to the driver
     ~DevBuf()
     {
         if (p)
             cudaFreeAsync(p, st);
+        if (p && trim_pool) {
+            cudaStreamSynchronize(st);
+            cudaMemPoolTrimTo(trim_pool, 64ull << 20);
+        }
     }
 };
 
@@ -512,32 +536,68 @@ struct Pinned {
 };
 thread_local Pinned t_pinned;
 
-void set_pool_threshold(int device)
+// The library's own stream-ordered pool per device (small control blocks, fetch scratch and
+// a library-allocated arena when cc_options.workspace is NULL).  Private, so that keeping freed
+// blocks cached (release threshold = max) never takes memory from torch or other users of the
+// device's default pool; the arena itself is trimmed back to the driver after every call.
+cudaMemPool_t lib_pool(int device)
 {
     static std::mutex mu;
-    static std::vector<int> done;
+    static std::vector<std::pair<int, cudaMemPool_t>> pools;
     std::lock_guard<std::mutex> lk(mu);
-    if (std::find(done.begin(), done.end(), device) != done.end())
-        return;
-    cudaMemPool_t pool;
-    if (cudaDeviceGetDefaultMemPool(&pool, device) == cudaSuccess) {
+    for (auto &p : pools)
+        if (p.first == device)
+            return p.second;
+    cudaMemPoolProps props{};
+    props.allocType = cudaMemAllocationTypePinned;
+    props.location.type = cudaMemLocationTypeDevice;
+    props.location.id = device;
+    cudaMemPool_t pool = nullptr;
+    if (cudaMemPoolCreate(&pool, &props) != cudaSuccess) {
+        cudaGetLastError();
+        cudaDeviceGetDefaultMemPool(&pool, device);
+    } else {
         u64 thr = ~0ull;
         cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
     }
-    done.push_back(device);
+    pools.push_back({device, pool});
+    return pool;
+}
+
+cudaError_t pool_alloc(void **p, size_t bytes, int device, cudaStream_t st)
+{
+    return cudaMallocFromPoolAsync(p, bytes, lib_pool(device), st);
 }
 
 // One frontier level F_t: a list of arena pages, all full except the last.
 struct Level {
     std::vector<uint32_t> pages;
     u64 count = 0;
-    bool sharded = false;   // paths already partitioned between shards (owned by this one)
-    bool init = false;      // sharded flag fixed (at the level's first write)
+    bool sharded = false;   // paths already partitioned between shards (owned by this one);
+                            // set whenever the level is (re)filled: from its parent at commit,
+                            // or from a Stage-1 chunk
     double fan = 0;         // observed extensions per path at this level (0 = unknown)
     bool shard_now = false; // unsharded level whose expansion does not fit: partition it first
 };
 
 }  // namespace
+
+// Copy records [from, from + cnt) of arena page `src` to slots [0, cnt) of page `dst`:
+// structure-of-arrays pages (record_bytes / 8 word arrays of P words, then a u32 ids array when
+// record_bytes % 8 == 4) or, for the wide class, array-of-structures records.
+static cudaError_t copy_records(char *base, u64 page_bytes, uint32_t lp, u64 rec_bytes, bool aos, uint32_t src,
+                                u64 from, u64 cnt, uint32_t dst, cudaStream_t st)
+{
+    const u64 P = 1ull << lp;
+    char *ps = base + (u64)src * page_bytes, *pd = base + (u64)dst * page_bytes;
+    if (aos)
+        return cudaMemcpyAsync(pd, ps + from * rec_bytes, cnt * rec_bytes, cudaMemcpyDeviceToDevice, st);
+    const u64 words = rec_bytes / 8;
+    cudaError_t e = cudaMemcpy2DAsync(pd, P * 8, ps + from * 8, P * 8, cnt * 8, words, cudaMemcpyDeviceToDevice, st);
+    if (e == cudaSuccess && rec_bytes % 8)
+        e = cudaMemcpyAsync(pd + words * P * 8, ps + words * P * 8 + from * 4, cnt * 4, cudaMemcpyDeviceToDevice, st);
+    return e;
+}
 
 static cc_status enumerate_impl(const cc_graph *cg, const cc_options *opt_in, cc_result **out,
                                 u64 *need_cycles)
@@ -597,7 +657,6 @@ static cc_status enumerate_impl(const cc_graph *cg, const cc_options *opt_in, cc
     }
     int sms = 0;
     CC_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device));
-    set_pool_threshold(device);
 
     DevCopy *dc = nullptr;
     {
@@ -638,7 +697,8 @@ static cc_status enumerate_impl(const cc_graph *cg, const cc_options *opt_in, cc
             CC_CUDA(cudaMemGetInfo(&fr, &tot));
             ws_bytes = std::max<u64>(fr / 4, 64ull << 20);
         }
-        CC_CUDA(cudaMallocAsync(&ws_own.p, ws_bytes, st));
+        CC_CUDA(pool_alloc(&ws_own.p, ws_bytes, device, st));
+        ws_own.trim_pool = lib_pool(device);
         ws = ws_own.p;
     }
     uint32_t lp = 20;  // 1 Mi records per page, fewer if the arena would have < 64 pages
@@ -660,7 +720,7 @@ static cc_status enumerate_impl(const cc_graph *cg, const cc_options *opt_in, cc
     DevBuf ctrl;
     ctrl.st = st;
     const size_t ctrl_bytes = sizeof(cc::Scratch) + (size_t)2 * npages * 4 + 256;
-    CC_CUDA(cudaMallocAsync(&ctrl.p, ctrl_bytes, st));
+    CC_CUDA(pool_alloc(&ctrl.p, ctrl_bytes, device, st));
     CC_CUDA(cudaMemsetAsync(ctrl.p, 0, sizeof(cc::Scratch), st));
     cc::Scratch *d_sc = (cc::Scratch *)ctrl.p;
     uint32_t *d_tab = (uint32_t *)((char *)ctrl.p + sizeof(cc::Scratch));
@@ -851,14 +911,13 @@ static cc_status enumerate_impl(const cc_graph *cg, const cc_options *opt_in, cc
     };
 
     std::vector<Level> levels(n + 3);
-    const bool count_tri = opt.shard_index == 0 && (opt.root_stride <= 1 || opt.root_offset == 0);
+    const bool count_tri = opt.shard_index == 0 && (opt.root_stride <= 1 || opt.root_offset == 0) &&
+                           (max_len == 0 || max_len >= 3);
     const u64 stage1_total = g->pair_prefix[n];
     S.stage1_pairs = stage1_total;
     u64 s1_next = 0;
     // shard at Stage 1 when the seed space alone is large enough (deterministic: graph-only)
     const bool s1_filter = W > 1 && stage1_total >= s1_shard_threshold;
-    levels[3].init = true;
-    levels[3].sharded = W == 1 || s1_filter;
     int deepest = 2;  // levels 3..deepest may be non-empty
     // small-frontier fast path (cc::SmallArgs): count mode, bitset records, n <= 128, one shard
     const bool small_ok = mode == cc::Mode::B && !wide && !list && nw <= 2 && W == 1 &&
@@ -890,6 +949,8 @@ static cc_status enumerate_impl(const cc_graph *cg, const cc_options *opt_in, cc
             Level &L3 = levels[3];
             L3.pages = used;
             L3.count = h_sc->out_count;
+            L3.sharded = W == 1 || s1_filter;  // a refill: earlier chunks' flags do not carry over
+            L3.shard_now = false;
             in_use += L3.count;
             high_water = std::max(high_water, in_use);
             deepest = 3;
@@ -905,7 +966,7 @@ static cc_status enumerate_impl(const cc_graph *cg, const cc_options *opt_in, cc
             const size_t na = (size_t)n + 3;
             DevBuf sm;
             sm.st = st;
-            CC_CUDA(cudaMallocAsync(&sm.p, (3 * na + 3) * 8, st));
+            CC_CUDA(pool_alloc(&sm.p, (3 * na + 3) * 8, device, st));
             CC_CUDA(cudaMemsetAsync(sm.p, 0, (3 * na + 3) * 8, st));
             u64 *d_count = (u64 *)sm.p, *d_cyc = d_count + na, *d_cand = d_cyc + na, *d_misc = d_cand + na;
             const u64 c3 = L.count;
@@ -967,8 +1028,8 @@ static cc_status enumerate_impl(const cc_graph *cg, const cc_options *opt_in, cc
             Level &N = levels[last];
             N.pages.assign(1, keep);
             N.count = hc[last];
-            N.init = true;
-            N.sharded = true;
+            N.sharded = true;  // W == 1 only
+            N.shard_now = false;
             in_use += N.count;
             high_water = std::max(high_water, in_use);
             if (N.count == 0) {
@@ -1004,11 +1065,9 @@ static cc_status enumerate_impl(const cc_graph *cg, const cc_options *opt_in, cc
         const bool emit = max_len == 0 || (u64)d + 1 < max_len;
         const bool leaf = emit && mode == cc::Mode::B && max_len != 0 && (u64)d + 2 >= max_len;
         const bool writes = emit && !leaf;
+        // F_{d+1} is empty here (d is the deepest non-empty level); its flags are set when this
+        // expansion commits, never before the launch (an overflow may still shard F_d first)
         Level &C = levels[d + 1];
-        if (writes && !C.init) {
-            C.init = true;
-            C.sharded = L.sharded;
-        }
         // ---- choose the input chunk: the last k pages of F_d
         size_t k = L.pages.size();
         if (writes && (W == 1 || L.sharded)) {
@@ -1029,13 +1088,32 @@ static cc_status enumerate_impl(const cc_graph *cg, const cc_options *opt_in, cc
             else
                 k = 1 + (size_t)((take - last_fill) / P);
         }
+        u64 sub = 0;  // > 0: expand only the last `sub` records of the last page (see below)
         for (;;) {
             const u64 last_fill = L.count - (u64)(L.pages.size() - 1) * P;
-            const u64 c = last_fill + (u64)(k - 1) * P;
+            u64 c = last_fill + (u64)(k - 1) * P;
             const uint32_t *in = L.pages.data() + (L.pages.size() - k);
+            // Less than one page: the tail [last_fill - sub, last_fill) of the last page is copied
+            // to a free page of its own and expanded from there; the level keeps the head, so its
+            // "all pages full but the last" layout is unchanged.  This is what keeps a tiny arena
+            // making progress when one page of a high fan-out level has more children than the
+            // free pages hold.
+            uint32_t tail_page = UINT32_MAX;
+            if (sub) {
+                if (free_pages.size() < 2)
+                    return fail(CC_ERR_CAPACITY, "workspace too small: no page to split F_" + std::to_string(d));
+                tail_page = free_pages.back();
+                free_pages.pop_back();
+                CC_CUDA(copy_records(base.pg.base, page_bytes, lp, rec_bytes, wide, L.pages.back(), last_fill - sub,
+                                     sub, tail_page, st));
+                in = &tail_page;
+                c = sub;
+            }
             bool of = false;
             trace_level = d;
-            cc_status s = launch(EXPAND, in, k, c, 0, emit, leaf, owner, false, used, &of);
+            cc_status s = launch(EXPAND, in, 1 + (sub ? 0 : k - 1), c, 0, emit, leaf, owner, false, used, &of);
+            if (tail_page != UINT32_MAX)
+                free_pages.push_back(tail_page);  // a copy: the records still live in L's last page
             if (s != CC_OK)
                 return s;
             if (of) {
@@ -1045,11 +1123,17 @@ static cc_status enumerate_impl(const cc_graph *cg, const cc_options *opt_in, cc
                     L.shard_now = true;
                     break;
                 }
-                if (k == 1)
-                    return fail(CC_ERR_CAPACITY, "workspace too small: one page of F_" + std::to_string(d) +
-                                                     " needs " + std::to_string(h_sc->out_count) +
-                                                     " output records, " + std::to_string(free_pages.size() * P) +
-                                                     " free");
+                if (k == 1) {
+                    if (c <= 1)
+                        return fail(CC_ERR_CAPACITY, "workspace too small: one path of F_" + std::to_string(d) +
+                                                         " needs " + std::to_string(h_sc->out_count) +
+                                                         " output records, " +
+                                                         std::to_string(free_pages.size() * P) + " free");
+                    L.fan = std::max(L.fan, (double)h_sc->out_count / (double)c);
+                    const double room = (double)(free_pages.size() - 1) * P;
+                    sub = std::max<u64>(1, std::min<u64>(c / 2, (u64)(room / (L.fan * 1.15))));
+                    continue;
+                }
                 L.fan = std::max(L.fan, (double)h_sc->out_count / (double)c);
                 const double room = (double)free_pages.size() * P;
                 const double want = room / (L.fan * 1.15);
@@ -1077,15 +1161,18 @@ static cc_status enumerate_impl(const cc_graph *cg, const cc_options *opt_in, cc
             S.bytes_alg += (c + h_sc->out_count) * rec_bytes;
             if (c > 0)
                 L.fan = (double)h_sc->out_count / (double)c;
-            for (size_t i = 0; i < k; ++i) {
-                free_pages.push_back(L.pages.back());
-                L.pages.pop_back();
-            }
+            if (!sub)
+                for (size_t i = 0; i < k; ++i) {
+                    free_pages.push_back(L.pages.back());
+                    L.pages.pop_back();
+                }
             L.count -= c;
             in_use -= c;
             if (h_sc->out_count) {
                 C.pages = used;
                 C.count = h_sc->out_count;
+                C.sharded = L.sharded || W == 1;
+                C.shard_now = false;
                 in_use += C.count;
                 high_water = std::max(high_water, in_use);
                 deepest = d + 1;
@@ -1215,7 +1302,7 @@ extern "C" cc_status cc_fetch_cycles(const cc_result *r, uint64_t first, uint64_
     cudaStream_t st = nullptr;
     // scratch from the stream-ordered pool (reused across batches, no device-wide sync)
     uint32_t *d_len = nullptr;
-    CC_CUDA(cudaMallocAsync(&d_len, cnt * 4, st));
+    CC_CUDA(pool_alloc((void **)&d_len, cnt * 4, r->device, st));
     std::vector<uint32_t> len(cnt);
     cudaError_t e = cc::launch_cycle_lengths(r->cyc, r->nw, first, cnt, d_len, st);
     if (e == cudaSuccess)
@@ -1233,8 +1320,8 @@ extern "C" cc_status cc_fetch_cycles(const cc_result *r, uint64_t first, uint64_
         return fail(CC_ERR_BUFFER_TOO_SMALL, "vertices needs " + std::to_string(total) + " entries");
     u64 *d_off = nullptr;
     int32_t *d_v = nullptr;
-    CC_CUDA(cudaMallocAsync(&d_off, (cnt + 1) * 8, st));
-    e = cudaMallocAsync(&d_v, std::max<u64>(total, 1) * 4, st);
+    CC_CUDA(pool_alloc((void **)&d_off, (cnt + 1) * 8, r->device, st));
+    e = pool_alloc((void **)&d_v, std::max<u64>(total, 1) * 4, r->device, st);
     if (e == cudaSuccess)
         e = cudaMemcpyAsync(d_off, offsets, (cnt + 1) * 8, cudaMemcpyHostToDevice, st);
     if (e == cudaSuccess)

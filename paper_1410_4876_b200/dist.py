@@ -45,6 +45,18 @@ def max_over_ranks(x: float, device=None, group=None) -> float:
     return float(t.item())
 
 
+def min_over_ranks(x: float, device=None, group=None) -> float:
+    """MIN of a scalar (e.g. the arena size every rank must share, include/chordless.h)."""
+    import torch
+    import torch.distributed as dist
+
+    t = torch.tensor([float(x)], dtype=torch.float64)
+    if device is not None:
+        t = t.to(device)
+    dist.all_reduce(t, op=dist.ReduceOp.MIN, group=group)
+    return float(t.item())
+
+
 def gather_per_rank(values, device=None, group=None):
     """All ranks' small float vectors (e.g. [device ms, paths]) for the imbalance report,
     SURVEY §8(e) -- reporting only, not on the data path."""

@@ -7,6 +7,7 @@ wall time and thread count of the run.  These are the expected values of the ful
 parity tests for workloads too large to run the oracle inside the test suite.
 """
 import argparse
+import hashlib
 import json
 import os
 import sys
@@ -52,6 +53,9 @@ def main():
         "paths_total": int(r["paths_by_len"].sum()), "candidates": r["candidates"],
         "oracle_seconds": dt, "oracle_threads": a.threads, "split_len": cfg.get("split_len", 8),
         "generated_by": "tests/golden/make_oracle_big.py (oracle/ only)",
+        # the input graph itself, so a change of the generator (e.g. numpy's PCG64 stream) is
+        # caught as a different graph rather than as a wrong count
+        "csr_sha256": hashlib.sha256(g[1].astype("<i8").tobytes() + g[2].astype("<i4").tobytes()).hexdigest(),
     }
     with open(os.path.join(HERE, f"oracle_{a.name}.json"), "w") as f:
         json.dump(out, f, indent=1)

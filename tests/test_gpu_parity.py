@@ -478,3 +478,32 @@ def test_degenerate_and_extreme_graphs(ws, name, g, K):
         assert int(got["counts"][700]) == 1 and int(got["counts"].sum()) == 1
     if name == "complete40":
         assert int(got["counts"][3]) == math.comb(40, 3) and int(got["counts"].sum()) == math.comb(40, 3)
+
+
+@pytest.mark.parametrize("W", [2, 3])
+def test_shard_fallback_when_an_unsharded_level_does_not_fit(ws, W):
+    """an unsharded level whose children overflow the arena is partitioned
+    on the spot (shard_now).  Its child level must inherit the partition that the COMMITTED
+    expansion used, so the shard sums still equal the whole.  A small arena and a huge
+    min_shard_paths make every split happen through that fallback."""
+    import torch
+    g = I.grid(7, 8)
+    small = torch.empty(160 * 1024 * 20, dtype=torch.uint8, device="cuda")
+    full = oracle.enumerate_cycles(*g, nthreads=NT)
+    parts = [binding.enumerate_cycles(*g, workspace=small, shard_index=i, shard_count=W,
+                                      min_shard_paths=1 << 30) for i in range(W)]
+    assert sum(p["counts"] for p in parts).tolist() == full["counts"].tolist()
+    assert sum(p["set_hash"] for p in parts) % (1 << 64) == full["set_hash"]
+    assert sum(p["paths_by_len"] for p in parts).tolist() == full["paths_by_len"].tolist()
+    assert sum(p["candidates"] for p in parts) == full["candidates"]
+    assert all(int(p["paths_by_len"].sum()) > 0 for p in parts)
+
+
+@pytest.mark.parametrize("K", [1, 2])
+def test_max_len_below_three_counts_nothing(ws, K):
+    """a cap below 3 vertices admits no cycle, not even a triangle."""
+    g = I.complete(6)
+    got = gpu(g, ws, max_len=K)
+    want = oracle.enumerate_cycles(*g, max_len=K)
+    assert int(got["counts"].sum()) == 0 == int(want["counts"].sum())
+    assert_same(got, want)

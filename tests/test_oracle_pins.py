@@ -449,3 +449,32 @@ def test_split_driver_equals_sequential_oracle(name, g, K, L):
     assert a["set_hash"] == b["set_hash"]
     assert a["paths_by_len"].tolist() == b["paths_by_len"].tolist()
     assert a["candidates"] == b["candidates"]
+
+
+def test_grid8x10_golden_equals_table1():
+    """Default-tier pin of the Table 1 Grid 8x10 row (PAPER.md:419, 71,535,910 chordless cycles
+    with more than 3 vertices, no triangles): the full oracle run behind
+    tests/golden/oracle_grid8x10.json (make_oracle_big.py, oracle/ only) reproduces it.  The
+    oracle run itself takes minutes, so it is rerun only in the slow tier (test_table1_counts)."""
+    import json
+    rows = {r[0]: r for r in _table1_rows()}
+    _, _, _, n, m, _, c3, clc = rows["Grid_8x10"]
+    d = json.load(open(os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden", "oracle_grid8x10.json")))
+    assert (d["n"], d["m"], d["max_len"]) == (n, m, 0)
+    assert int(d["counts"].get("3", 0)) == c3
+    assert d["total"] - int(d["counts"].get("3", 0)) == clc
+    assert sum(d["counts"].values()) == d["total"]
+
+
+def test_gnp2000_generator_is_the_golden_graph():
+    """configs[3]'s graph is pinned by digest: the K = 9 / K = 10 goldens were computed on the
+    CSR whose SHA-256 they store.  A change of the generator (e.g. numpy's PCG64 stream) fails
+    here instead of silently turning the goldens into statements about another graph."""
+    import hashlib
+    import json
+    n, rp, col = I.gnp(2000, 0.005, I.GNP_SEED)
+    digest = hashlib.sha256(rp.astype("<i8").tobytes() + col.astype("<i4").tobytes()).hexdigest()
+    for name in ("gnp2000_k9", "gnp2000_k10"):
+        d = json.load(open(os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden", f"oracle_{name}.json")))
+        assert d["csr_sha256"] == digest
+        assert (d["n"], d["m"]) == (n, len(col) // 2)
