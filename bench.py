@@ -362,13 +362,18 @@ def main():
     st_last = stats[-1]
     t_expand = sum(s["t_expand_ms"] for s in stats)
     rec_b = st_last["record_bytes"]
-    records_moved = sum(s["bytes_alg"] for s in stats) / rec_b if rec_b else 0.0
+    # per path expanded R_in + s*R_out, i.e. every expanded path read once and every
+    # child written once, as a level-synchronous expansion does (records_levelsync)
+    records_alg = sum(s["records_levelsync"] for s in stats)
     r_alg = r_alg_bytes(g[0], st_last["record_format"])
-    bytes_alg = records_moved * r_alg
+    bytes_alg = records_alg * r_alg
+    # what the launches really move: slots read + written (incl. empty chunk slots) at the stored
+    # record size -- half of the above or less where two levels run per launch
+    bytes_moved = sum(s["slots_moved"] for s in stats) * rec_b
     launches = sum(s["launches"] for s in stats)
     peak, peak_kind = peaks()
     achieved = (bytes_alg / (t_expand / 1e3)) / 1e9 if t_expand > 0 else 0.0
-    achieved_rec = (records_moved * rec_b / (t_expand / 1e3)) / 1e9 if t_expand > 0 else 0.0
+    achieved_moved = (bytes_moved / (t_expand / 1e3)) / 1e9 if t_expand > 0 else 0.0
     # traffic: dram__bytes_read.sum + dram__bytes_write.sum of one ncu --set full capture of this
     # kernel (one launch, profiles/ncu_traffic.json), against that launch's R_alg bytes
     traffic = traffic_ratio = traffic_src = None
@@ -387,12 +392,12 @@ def main():
                 "frac": achieved / peak, "traffic": traffic, "traffic_over_alg": traffic_ratio,
                 "traffic_source": traffic_src, "peak_kind": peak_kind,
                 "r_alg_bytes": r_alg, "record_bytes": rec_b,
-                "achieved_record_bytes": achieved_rec, "frac_record_bytes": achieved_rec / peak,
+                "achieved_moved": achieved_moved, "frac_moved": achieved_moved / peak,
                 "kernel": ("k_expand_blocked" if g[0] <= 512 else
                            "k_expand_list" if st_last["record_format"] == 2 else "k_expand_wide"),
                 "expand_share_of_step": t_expand / dev_ms if dev_ms else None,
-                "records_per_step": records_moved / args.steps,
-                "bytes_alg_per_step": bytes_alg / args.steps}
+                "records_alg_per_step": records_alg / args.steps,
+                "bytes_alg_per_step": bytes_alg / args.steps, "bytes_moved_per_step": bytes_moved / args.steps}
     if st_last["record_format"] == 2:
         # vertex-list records (24 B) move so few bytes that HBM is not the bound: the time goes
         # to random 4-byte reads of the neighbour-mask table in L2

@@ -112,8 +112,8 @@ typedef struct {
     uint64_t peak_arena_records;  /* high-water mark of the frontier arena, in records */
     uint64_t arena_capacity;      /* arena capacity, in records */
     uint64_t record_bytes;        /* bytes per frontier record */
-    uint64_t bytes_alg;           /* algorithmic bytes moved by the expansion kernels
-                                     (records read + records written + cycles stored) */
+    uint64_t bytes_alg;           /* bytes of the records the expansion kernels read and write
+                                     (real records, at record_bytes each) + cycles stored */
     uint64_t cycles_stored;       /* collect mode: cycles kept (or required, on overflow) */
     uint64_t h2d_bytes;           /* host->device bytes this call (graph upload, if any) */
     uint64_t d2h_bytes;           /* device->host bytes this call (counts, sizes) */
@@ -128,6 +128,13 @@ typedef struct {
     uint64_t paths_written;       /* frontier records written by Stage 1 and Stage 2 */
     uint64_t record_format;       /* frontier records used: 1 = blocked set (or bitmap S in
                                      collect mode), 2 = vertex list (cc_options.record_format) */
+    uint64_t records_levelsync;   /* records a level-synchronous expansion of the same paths reads
+                                     and writes: every expanded path once, every child once
+                                     (SURVEY §8(d) "R_in + s*R_out" per path expanded).  The grid
+                                     class's two-level launches keep every other level in shared
+                                     memory and move fewer (bytes_alg) */
+    uint64_t slots_moved;         /* frontier slots read + written by Stage 2 launches, including
+                                     the empty slots of per-warp output chunks */
 } cc_stats;
 
 /* Fills *opt with defaults (device -1, stream NULL, no cap, count-only, one shard). */

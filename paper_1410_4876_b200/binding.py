@@ -63,7 +63,8 @@ class cc_stats(ctypes.Structure):
         ("t_expand_ms", ctypes.c_double), ("t_stage1_ms", ctypes.c_double),
         ("t_labeling_ms", ctypes.c_double), ("t_wall_ms", ctypes.c_double),
         ("leaf_paths", ctypes.c_uint64), ("paths_written", ctypes.c_uint64),
-        ("record_format", ctypes.c_uint64),
+        ("record_format", ctypes.c_uint64), ("records_levelsync", ctypes.c_uint64),
+        ("slots_moved", ctypes.c_uint64),
     ]
 
 

@@ -1,4 +1,7 @@
-"""Build libchordless.so (the C-ABI library) in-tree with nvcc for sm_100a."""
+"""Build libchordless.so (the C-ABI library) in-tree with nvcc for sm_100a.
+
+Each translation unit is compiled to an object in parallel (nvcc -c), then linked into one
+shared library with the static CUDA runtime."""
 from __future__ import annotations
 
 import os
@@ -9,12 +12,12 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
 ROOT = os.path.dirname(HERE)
 LIB = os.path.join(HERE, "libchordless.so")
-SOURCES = [os.path.join(CSRC, "cc_kernels.cu"), os.path.join(CSRC, "cc_host.cpp")]
-HEADERS = [os.path.join(CSRC, "cc_internal.h"), os.path.join(ROOT, "include", "chordless.h")]
+SOURCES = [os.path.join(CSRC, f) for f in ("cc_kernels.cu", "cc_fused.cu", "cc_host.cpp")]
+HEADERS = [os.path.join(CSRC, f) for f in ("cc_internal.h", "cc_device.cuh")] + [os.path.join(ROOT, "include", "chordless.h")]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
-FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-shared", "-Xcompiler", "-fPIC,-O2", "-cudart", "static",
-         "-I", os.path.join(ROOT, "include")]
+CFLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC,-O2", "-I", os.path.join(ROOT, "include")]
+EXTRA = os.environ.get("CC_NVCC_FLAGS", "").split()  # A/B builds (e.g. -DCC_EB_R=1)
 
 
 def stale() -> bool:
@@ -26,12 +29,29 @@ def stale() -> bool:
 
 def build(force: bool = False, verbose: bool = False) -> str:
     if force or stale():
-        tmp = LIB + f".tmp{os.getpid()}"
-        cmd = [NVCC, *ARCH, *FLAGS, *SOURCES, "-o", tmp]
-        if verbose:
-            print(" ".join(cmd), file=sys.stderr)
-        subprocess.check_call(cmd)
-        os.replace(tmp, LIB)
+        tag = f".tmp{os.getpid()}"
+        objs, procs = [], []
+        for src in SOURCES:
+            obj = os.path.join(CSRC, os.path.basename(src) + tag + ".o")
+            cmd = [NVCC, *ARCH, *CFLAGS, *EXTRA, "-c", src, "-o", obj]
+            if verbose:
+                print(" ".join(cmd), file=sys.stderr)
+            procs.append(subprocess.Popen(cmd))
+            objs.append(obj)
+        try:
+            for p in procs:
+                if p.wait() != 0:
+                    raise subprocess.CalledProcessError(p.returncode, p.args)
+            tmp = LIB + tag
+            cmd = [NVCC, *ARCH, "-shared", "-cudart", "static", *objs, "-o", tmp]
+            if verbose:
+                print(" ".join(cmd), file=sys.stderr)
+            subprocess.check_call(cmd)
+            os.replace(tmp, LIB)
+        finally:
+            for o in objs:
+                if os.path.exists(o):
+                    os.remove(o)
     return LIB
 
 

@@ -1,0 +1,511 @@
+// cc_fused.cu -- k_expand_fused: Stage 2 (Alg. 3) of count mode for the
+// grid class (bitset blocked-set records of NW <= 2 words, n <= 128, max degree <= 4), the
+// HBM-bound workloads of SURVEY §8(d) (P8x8, P10x10 and the Table 1 grids).
+//
+// Two levels per launch.  The paper writes every frontier T' to global memory and relaunches
+// (Alg. 4 l.4-7); here a launch reads F_t and writes F_{t+2}: the children
+// <p,v> (F_{t+1}) live only in shared memory, where they are tested for closures and expanded
+// in turn.  Per path the test is the one of k_expand_blocked (cc_kernels.cu), the dichotomy of
+// PAPER.md:57-64 on the blocked-vertex record B(p) = N[v2] u ... u N[v_{t-1}]:
+//   Cand = Adj(vt) & {v > v2} & ~B,  Close = Cand & Adj(v1),  Ext = Cand & ~Adj(v1)
+//   child <p,v>: B' = B | N[vt], keysum' = keysum + key(v), ids' = (v1, v2, v).
+// FUSE = 1 is the single-level form (last levels under a length cap; LEAF = last-level fusion).
+//
+// Warps are independent: no block-wide barrier inside the tile loop.  A warp takes tiles of 32
+// consecutive input records (one per lane, loaded with coalesced 256-byte accesses, the next
+// tile prefetched into registers), stages its children (and grandchildren) in its own slice of
+// shared memory, and stores them with coalesced, consecutive-slot writes.  Output positions come
+// from per-warp chunks of 2^log_ch slots (one atomicAdd per chunk, not per tile: the paper's
+// serialized index allocation, amortised over a chunk).  The unused tail of a
+// warp's last chunk is written as all-zero records ("empty slots": v1 == v2 == 0, which no path
+// has), which every reader of such a level skips (k_expand_fused, k_expand_blocked,
+// k_shard_filter); empty slots are at most warps x 2^log_ch per launch and the host sizes
+// log_ch so that this is a small fraction of the launch's output.
+#include "cc_device.cuh"
+
+#include <algorithm>
+
+namespace cc {
+
+constexpr int kFBlock = 256;             // 8 independent warps; the CTA shares the graph tables
+constexpr int kFWarps = kFBlock / 32;
+constexpr int kFMaxCh = 3;               // Delta <= 4: at most 3 children per path
+constexpr int kFCh1 = 32 * kFMaxCh;      // children of one warp tile
+constexpr int kFCh2 = kFCh1 * kFMaxCh;   // grandchildren of one warp tile
+
+template <int NW, bool PACK, int FUSE>
+struct FusedWarpSmem {
+    static constexpr int PW = 2 * NW + 1;               // B | N[vt] (NW), keysum, Ext (NW)
+    u64 par[32][PW];                                    // level-t parents with children
+    u64 par2[FUSE == 2 ? kFCh1 : 1][PW];                // level-(t+1) children with children
+    uint32_t pid[PACK ? 1 : 32];                        // unpacked ids: v1 | v2 << 10
+    uint32_t pid2[(PACK || FUSE == 1) ? 1 : kFCh1];
+    uint8_t ent1[kFCh1];                                // child k: parent lane | rank << 5
+    uint16_t ent2[FUSE == 2 ? kFCh2 : 1];               // grandchild k: child index | rank << 7
+};
+
+template <int NW, bool PACK, int FUSE>
+__host__ __device__ constexpr size_t fused_warp_bytes()
+{
+    return (sizeof(FusedWarpSmem<NW, PACK, FUSE>) + 15) & ~(size_t)15;
+}
+
+// rank-th (rank < 3) set bit of the NW-word set x
+template <int NW>
+__device__ __forceinline__ uint32_t select_bit(const u64 (&x)[NW], uint32_t rank)
+{
+    u64 w = x[0];
+    uint32_t wsel = 0;
+#pragma unroll
+    for (int i = 1; i < NW; ++i) {
+        const uint32_t pc = __popcll(w);
+        const bool next = rank >= pc;
+        rank = next ? rank - pc : rank;
+        wsel = next ? (uint32_t)i : wsel;
+        w = next ? x[i] : w;
+    }
+#pragma unroll
+    for (int c = 1; c < kFMaxCh; ++c) {
+        const u64 y = w & (w - 1);
+        w = (uint32_t)c <= rank ? y : w;
+    }
+    return 64 * wsel + (uint32_t)__ffsll((long long)w) - 1;
+}
+
+// Per-warp output cursor over chunks of 2^log_ch slots (warp-uniform state).
+struct WarpOut {
+    u64 pos = 0;          // next free slot of the current chunk
+    uint32_t left = 0;    // free slots left in it
+    bool dead = false;    // output overflow: the launch is discarded by the host
+};
+
+// Reserve T slots (warp-uniform T): slots k < split are pos0 + k, the others pos1 + (k - split).
+__device__ __forceinline__ void warp_reserve(WarpOut &o, uint32_t T, uint32_t log_ch, const LaunchArgs &p,
+                                             u64 &pos0, u64 &pos1, uint32_t &split)
+{
+    pos0 = o.pos;
+    pos1 = 0;
+    split = T;
+    if (T <= o.left) {
+        o.pos += T;
+        o.left -= T;
+        return;
+    }
+    const uint32_t need = T - o.left;
+    const u64 nch = ((u64)need + (1u << log_ch) - 1) >> log_ch;
+    u64 nb = 0;
+    if ((threadIdx.x & 31) == 0)
+        nb = atomicAdd(&p.sc->out_count, nch << log_ch);
+    nb = __shfl_sync(FULL_MASK, nb, 0);
+    if (nb + (nch << log_ch) > p.out_cap) {
+        if ((threadIdx.x & 31) == 0)
+            p.sc->err = 1;
+        o.dead = true;
+        o.left = 0;
+        return;
+    }
+    split = o.left;
+    pos1 = nb;
+    o.pos = nb + need;
+    o.left = (uint32_t)((nch << log_ch) - need);
+}
+
+// store record C (RW words, plus the ids word when unpacked) at virtual output position o
+template <int RW, bool PACK>
+__device__ __forceinline__ void put_record(const LaunchArgs &p, u64 o, const u64 (&C)[RW], uint32_t id)
+{
+    o += p.out_off;
+    char *pp = page_ptr(p.pg, p.pg.out_pages[o >> p.pg.log_p]);
+    const u64 slot = o & ((1ull << p.pg.log_p) - 1);
+    u64 *w0 = (u64 *)pp + slot;
+#pragma unroll
+    for (int w = 0; w < RW; ++w)
+        w0[(u64)w << p.pg.log_p] = C[w];
+    if (!PACK)
+        ((uint32_t *)(pp + ((u64)RW << p.pg.log_p) * 8))[slot] = id;
+}
+
+template <int NW, bool PACK, int FUSE, bool LEAF>
+__global__ void __launch_bounds__(kFBlock, 4) k_expand_fused(const LaunchArgs p, const uint32_t log_ch)
+{
+    static_assert(FUSE == 1 || !LEAF, "last-level fusion is single-level");
+    constexpr int RW = NW + 1;
+    using WS = FusedWarpSmem<NW, PACK, FUSE>;
+    extern __shared__ __align__(16) u64 smem[];
+    const int n = p.g.n;
+    u64 *s_adj = smem;                          // closed rows N[v] = Adj(v) | {v}
+    u64 *s_above = s_adj + n * NW;              // label gate {x : x > v}
+    u64 *s_key = s_above + n * NW;              // key(v)
+    char *wbase = (char *)(s_key + ((n + 1) & ~1));
+    WS &ws = *(WS *)(wbase + (threadIdx.x >> 5) * fused_warp_bytes<NW, PACK, FUSE>());
+    for (int i = threadIdx.x; i < n * NW; i += kFBlock) {
+        s_above[i] = above_word((uint32_t)(i / NW), i % NW);
+        s_adj[i] = p.g.adj[i] | bit_in_word(i % NW, (uint32_t)(i / NW));
+    }
+    for (int i = threadIdx.x; i < n; i += kFBlock)
+        s_key[i] = p.g.key[i];
+    __syncthreads();
+
+    const int lane = threadIdx.x & 31;
+    const uint32_t idb = PACK ? p.idb : (uint32_t)kIdBits;
+    const uint32_t idm = (1u << idb) - 1;
+    const uint32_t v12m = (1u << (2 * idb)) - 1;
+    const u64 keep_v12 = PACK ? ~((u64)idm << (64 - idb)) : ~0ull;  // packed: clears the vt field
+    const u64 P = 1ull << p.pg.log_p;
+    const u64 pmask = P - 1;
+    const u64 nt = (p.n_in + 31) >> 5;
+    const u64 tw = (u64)gridDim.x * kFWarps;
+    WarpOut out;
+    // per-lane statistics (a launch gives a lane at most ~10^6 paths)
+    uint32_t n_in = 0, cnt1 = 0, cand1 = 0, n_next = 0, cnt2 = 0, cand2 = 0, written = 0;
+    u64 hs = 0;
+
+    auto load = [&](u64 wt, u64 (&X)[RW], uint32_t &xid) {
+        const u64 r0 = wt << 5;
+        const char *pp = page_ptr(p.pg, p.pg.in_pages[r0 >> p.pg.log_p]);
+        const u64 slot = (r0 & pmask) + lane;
+#pragma unroll
+        for (int w = 0; w < RW; ++w)
+            X[w] = __ldcs((const u64 *)pp + ((u64)w << p.pg.log_p) + slot);  // read once: evict first
+        xid = PACK ? 0u : __ldcs((const uint32_t *)(pp + ((u64)RW << p.pg.log_p) * 8) + slot);
+    };
+    // copy T staged records to the warp's output slots (uniform loop, consecutive slots)
+    auto emit = [&](uint32_t T, bool second) {
+        if (T == 0 || out.dead)
+            return;
+        u64 pos0, pos1;
+        uint32_t split;
+        warp_reserve(out, T, log_ch, p, pos0, pos1, split);
+        if (out.dead)
+            return;
+        written += T;  // counted once per warp below (lane 0 share)
+        for (uint32_t k = lane; k < T; k += 32) {
+            uint32_t q, rank;
+            const u64 *par;
+            uint32_t pid = 0;
+            if (FUSE == 2 && second) {
+                const uint32_t e = ws.ent2[k];
+                q = e & 127;
+                rank = e >> 7;
+                par = ws.par2[q];
+                if (!PACK)
+                    pid = ws.pid2[q];
+            } else {
+                const uint32_t e = ws.ent1[k];
+                q = e & 31;
+                rank = e >> 5;
+                par = ws.par[q];
+                if (!PACK)
+                    pid = ws.pid[q];
+            }
+            u64 ex[NW];
+#pragma unroll
+            for (int w = 0; w < NW; ++w)
+                ex[w] = par[NW + 1 + w];
+            const uint32_t v = select_bit<NW>(ex, rank);
+            u64 C[RW];
+#pragma unroll
+            for (int w = 0; w < NW; ++w)
+                C[w] = par[w];
+            C[NW] = par[NW] + s_key[v];
+            if (PACK)
+                C[NW - 1] |= (u64)v << (64 - idb);
+            put_record<RW, PACK>(p, k < split ? pos0 + k : pos1 + (k - split), C, pid | (v << (2 * idb)));
+        }
+    };
+
+    u64 W[RW];
+    uint32_t id = 0;
+    u64 wt = blockIdx.x * (u64)kFWarps + (threadIdx.x >> 5);
+    if (wt < nt)
+        load(wt, W, id);
+    for (; wt < nt && !out.dead; wt += tw) {
+        u64 Wn[RW];
+        uint32_t idn = 0;
+        if (wt + tw < nt)
+            load(wt + tw, Wn, idn);
+        // ---------------------------------------------------------------- level t
+        const u64 r = (wt << 5) + lane;
+        const uint32_t ids = PACK ? (uint32_t)packed_ids(W[NW - 1], idb) : id;
+        const uint32_t v1 = ids & idm, v2 = (ids >> idb) & idm, vt = ids >> (2 * idb);
+        const bool valid = r < p.n_in && v1 != v2;  // v1 == v2: an empty slot
+        u64 ext[NW];
+        uint32_t nc = 0;
+#pragma unroll
+        for (int w = 0; w < NW; ++w)
+            ext[w] = 0;
+        if (valid) {
+            n_in++;
+            u64 arow[NW], abv[NW], a1[NW];
+            lds_row<NW>(s_adj, vt, arow);
+            lds_row<NW>(s_above, v2, abv);
+            lds_row<NW>(s_adj, v1, a1);
+            cand1 -= 1;  // deg(vt) = |N[vt]| - 1
+            u64 close[NW];
+            bool any_close = false;
+#pragma unroll
+            for (int w = 0; w < NW; ++w) {
+                cand1 += __popcll(arow[w]);
+                const u64 c = arow[w] & abv[w] & ~W[w];  // packed ids sit above bit n: not in arow
+                close[w] = c & a1[w];
+                ext[w] = p.emit ? (c & ~a1[w]) : 0ull;
+                any_close |= close[w] != 0ull;
+            }
+            if (any_close && p.count) {
+#pragma unroll
+                for (int w = 0; w < NW; ++w) {
+                    u64 m = close[w];
+                    cnt1 += __popcll(m);
+                    while (m) {
+                        const int b = __ffsll((long long)m) - 1;
+                        m &= m - 1;
+                        hs += mix64(W[NW] + s_key[64 * w + b]);
+                    }
+                }
+            }
+            if constexpr (LEAF) {
+                // children <p,v> are the last level: counted here, never written.
+                // Close(<p,v>) = Adj(v) & Z(p), Z(p) = {x > v2} & ~(B | N[vt]) & Adj(v1)
+                if (p.count) {
+                    u64 Z[NW];
+#pragma unroll
+                    for (int w = 0; w < NW; ++w)
+                        Z[w] = abv[w] & ~(W[w] | arow[w]) & a1[w];
+#pragma unroll
+                    for (int w = 0; w < NW; ++w) {
+                        u64 m = ext[w];
+                        while (m) {
+                            const int b = __ffsll((long long)m) - 1;
+                            m &= m - 1;
+                            const uint32_t v = (uint32_t)(64 * w + b);
+                            u64 av[NW];
+                            lds_row<NW>(s_adj, v, av);
+                            const u64 ksv = W[NW] + s_key[v];
+                            n_next++;
+                            cand2 -= 1;
+#pragma unroll
+                            for (int w2 = 0; w2 < NW; ++w2) {
+                                cand2 += __popcll(av[w2]);
+                                u64 cl = av[w2] & Z[w2];
+                                cnt2 += __popcll(cl);
+                                while (cl) {
+                                    const int b2 = __ffsll((long long)cl) - 1;
+                                    cl &= cl - 1;
+                                    hs += mix64(ksv + s_key[64 * w2 + b2]);
+                                }
+                            }
+                        }
+                    }
+                }
+#pragma unroll
+                for (int w = 0; w < NW; ++w)
+                    ext[w] = 0;
+            } else {
+#pragma unroll
+                for (int w = 0; w < NW; ++w)
+                    nc += __popcll(ext[w]);
+                if (nc) {
+                    // stage the parent: B | N[vt] (vt field cleared), keysum, Ext
+#pragma unroll
+                    for (int w = 0; w < NW; ++w)
+                        ws.par[lane][w] = (W[w] | arow[w]) & (w == NW - 1 ? keep_v12 : ~0ull);
+                    ws.par[lane][NW] = W[NW];
+#pragma unroll
+                    for (int w = 0; w < NW; ++w)
+                        ws.par[lane][NW + 1 + w] = ext[w];
+                    if (!PACK)
+                        ws.pid[lane] = ids & v12m;
+                }
+            }
+        }
+        // warp scan of the child counts -> each child's slot in ent1
+        uint32_t incl = nc;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const uint32_t x = __shfl_up_sync(FULL_MASK, incl, o);
+            if (lane >= o)
+                incl += x;
+        }
+        const uint32_t T1 = __shfl_sync(FULL_MASK, incl, 31);
+        {
+            const uint32_t off = incl - nc;
+#pragma unroll
+            for (uint32_t c = 0; c < (uint32_t)kFMaxCh; ++c)
+                if (c < nc)
+                    ws.ent1[off + c] = (uint8_t)(lane | (c << 5));
+        }
+        __syncwarp();
+        if constexpr (FUSE == 1) {
+            emit(T1, false);
+        } else {
+            // ------------------------------------------------------------ level t+1 (in smem)
+            uint32_t ng[kFMaxCh];
+#pragma unroll
+            for (int ro = 0; ro < kFMaxCh; ++ro) {
+                ng[ro] = 0;
+                const uint32_t j = 32 * ro + lane;
+                if (32 * (uint32_t)ro >= T1)
+                    continue;  // warp-uniform
+                if (j < T1) {
+                    const uint32_t e = ws.ent1[j];
+                    const uint32_t q = e & 31;
+                    u64 Bc[NW], ex[NW];
+#pragma unroll
+                    for (int w = 0; w < NW; ++w) {
+                        Bc[w] = ws.par[q][w];
+                        ex[w] = ws.par[q][NW + 1 + w];
+                    }
+                    const uint32_t v = select_bit<NW>(ex, e >> 5);
+                    const u64 ksc = ws.par[q][NW] + s_key[v];
+                    const uint32_t cid = PACK ? (uint32_t)packed_ids(Bc[NW - 1], idb) : ws.pid[q];
+                    const uint32_t c1 = cid & idm, c2 = (cid >> idb) & idm;
+                    n_next++;
+                    u64 arow[NW], abv[NW], a1[NW], ex2[NW];
+                    lds_row<NW>(s_adj, v, arow);
+                    lds_row<NW>(s_above, c2, abv);
+                    lds_row<NW>(s_adj, c1, a1);
+                    cand2 -= 1;
+                    uint32_t g = 0;
+#pragma unroll
+                    for (int w = 0; w < NW; ++w) {
+                        cand2 += __popcll(arow[w]);
+                        const u64 c = arow[w] & abv[w] & ~Bc[w];
+                        u64 cl = c & a1[w];
+                        ex2[w] = c & ~a1[w];
+                        g += __popcll(ex2[w]);
+                        if (p.count) {
+                            cnt2 += __popcll(cl);
+                            while (cl) {
+                                const int b = __ffsll((long long)cl) - 1;
+                                cl &= cl - 1;
+                                hs += mix64(ksc + s_key[64 * w + b]);
+                            }
+                        }
+                    }
+                    ng[ro] = g;
+                    if (g) {
+#pragma unroll
+                        for (int w = 0; w < NW; ++w)
+                            ws.par2[j][w] = Bc[w] | arow[w];  // v1, v2 stay in the packed bits
+                        ws.par2[j][NW] = ksc;
+#pragma unroll
+                        for (int w = 0; w < NW; ++w)
+                            ws.par2[j][NW + 1 + w] = ex2[w];
+                        if (!PACK)
+                            ws.pid2[j] = cid;
+                    }
+                }
+            }
+            // lane L owns children L, L+32, L+64: one contiguous block of grandchild slots
+            const uint32_t mine = ng[0] + ng[1] + ng[2];
+            uint32_t inc2 = mine;
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                const uint32_t x = __shfl_up_sync(FULL_MASK, inc2, o);
+                if (lane >= o)
+                    inc2 += x;
+            }
+            const uint32_t T2 = __shfl_sync(FULL_MASK, inc2, 31);
+            uint32_t off = inc2 - mine;
+#pragma unroll
+            for (int ro = 0; ro < kFMaxCh; ++ro) {
+                const uint32_t j = 32 * ro + lane;
+#pragma unroll
+                for (uint32_t c = 0; c < (uint32_t)kFMaxCh; ++c)
+                    if (c < ng[ro])
+                        ws.ent2[off + c] = (uint16_t)(j | (c << 7));
+                off += ng[ro];
+            }
+            __syncwarp();
+            emit(T2, true);
+        }
+        __syncwarp();  // the next tile overwrites par / ent
+#pragma unroll
+        for (int w = 0; w < RW; ++w)
+            W[w] = Wn[w];
+        id = idn;
+    }
+    // empty slots: the unused tail of the warp's last chunk
+    if (!out.dead && out.left) {
+        u64 Z[RW];
+#pragma unroll
+        for (int w = 0; w < RW; ++w)
+            Z[w] = 0;
+        for (uint32_t k = lane; k < out.left; k += 32)
+            put_record<RW, PACK>(p, out.pos + k, Z, 0u);
+    }
+    if (!p.count) {
+        cand1 = cand2 = 0;
+    }
+    Acc a;
+    a.cyc = cnt1;
+    a.hash = hs;
+    a.cand = cand1;
+    a.cyc_next = cnt2;
+    a.cand_next = cand2;
+    a.paths_next = n_next;
+    a.paths_cur = n_in;
+    a.out_real = lane == 0 ? written : 0;
+    flush<kFBlock>(a, p.sc);
+}
+
+template <int NW, bool PACK, int FUSE>
+static size_t fused_smem_t(int n)
+{
+    return ((size_t)n * 2 * NW + ((n + 1) & ~1)) * sizeof(u64) + kFWarps * fused_warp_bytes<NW, PACK, FUSE>();
+}
+
+size_t fused_smem(int nw, int n, bool packed, int fuse)
+{
+    if (nw == 1)
+        return packed ? (fuse == 2 ? fused_smem_t<1, true, 2>(n) : fused_smem_t<1, true, 1>(n))
+                      : (fuse == 2 ? fused_smem_t<1, false, 2>(n) : fused_smem_t<1, false, 1>(n));
+    return packed ? (fuse == 2 ? fused_smem_t<2, true, 2>(n) : fused_smem_t<2, true, 1>(n))
+                  : (fuse == 2 ? fused_smem_t<2, false, 2>(n) : fused_smem_t<2, false, 1>(n));
+}
+
+typedef void (*FusedFn)(const LaunchArgs, const uint32_t);
+
+static FusedFn fused_kernel(int nw, bool pk, int fuse, bool leaf)
+{
+#define FK(N, PK)                                                                          \
+    if (nw == N && pk == PK)                                                               \
+        return fuse == 2 ? k_expand_fused<N, PK, 2, false>                                 \
+                         : (leaf ? k_expand_fused<N, PK, 1, true> : k_expand_fused<N, PK, 1, false>);
+    FK(1, true) FK(1, false) FK(2, true) FK(2, false)
+#undef FK
+    return nullptr;
+}
+
+int fused_warps_per_launch(int nw, int n, bool packed, int fuse, bool leaf, int sms)
+{
+    FusedFn f = fused_kernel(nw, packed, fuse, leaf);
+    if (!f)
+        return 0;
+    const size_t smem = fused_smem(nw, n, packed, fuse);
+    if (cudaFuncSetAttribute((const void *)f, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess)
+        return 0;
+    int nb = 0;
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, (const void *)f, kFBlock, smem) != cudaSuccess)
+        return 0;
+    return nb * sms * kFWarps;
+}
+
+cudaError_t launch_fused(const LaunchArgs &a, int fuse, bool leaf, uint32_t log_ch, int max_warps, cudaStream_t st)
+{
+    FusedFn f = fused_kernel(a.g.nw, a.packed != 0, fuse, leaf);
+    if (!f || a.g.n > 128 || log_ch < 5 || max_warps < kFWarps)
+        return cudaErrorInvalidValue;
+    const size_t smem = fused_smem(a.g.nw, a.g.n, a.packed != 0, fuse);
+    cudaError_t e = cudaFuncSetAttribute((const void *)f, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess)
+        return e;
+    const u64 tiles = (a.n_in + 31) / 32;
+    u64 blocks = std::min<u64>((u64)max_warps / kFWarps, (tiles + kFWarps - 1) / kFWarps);
+    if (blocks == 0)
+        blocks = 1;
+    f<<<(unsigned)blocks, kFBlock, smem, st>>>(a, log_ch);
+    return cudaGetLastError();
+}
+
+}  // namespace cc

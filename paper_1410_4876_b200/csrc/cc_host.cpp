@@ -576,7 +576,9 @@ struct Level {
     bool sharded = false;   // paths already partitioned between shards (owned by this one);
                             // set whenever the level is (re)filled: from its parent at commit,
                             // or from a Stage-1 chunk
-    double fan = 0;         // observed extensions per path at this level (0 = unknown)
+    double fan = 0;         // observed output slots per input slot of this level's launches (0 = unknown)
+    int fan_fuse = -1;      // the launch kind `fan` was observed for (fuse 0 / 1 / 2)
+    double fan1 = 0;        // observed |F_{t+1}| / |F_t| (one level), 0 = unknown
     bool shard_now = false; // unsharded level whose expansion does not fit: partition it first
 };
 
@@ -776,6 +778,19 @@ static cc_status enumerate_impl(const cc_graph *cg, const cc_options *opt_in, cc
     const int grid_sf = (list ? cc::max_blocks_per_sm_list(2, rwl)
                          : wide ? cc::max_blocks_per_sm_wide(2) : cc::max_blocks_per_sm(3, mode, nw, packed, 0)) * sms;
     const double maxfan = (double)std::max<int64_t>(g->max_deg - 1, 1);
+    // Grid class (count mode, bitset records of <= 2 words, max degree <= 4): large levels are
+    // expanded by k_expand_fused (cc_fused.cu), two levels per launch where the length cap allows
+    const bool fused_ok = mode == cc::Mode::B && !wide && !list && nw <= 2 && n <= 128 && g->max_deg <= 4 &&
+                          std::getenv("CC_NO_FUSED") == nullptr;
+    const u64 fused_min = std::getenv("CC_FUSED_MIN") ? std::strtoull(std::getenv("CC_FUSED_MIN"), nullptr, 10)
+                                                       : (1ull << 20);
+    int fused_warps[3] = {-1, -1, -1};  // resident warps of the fused kernel: fuse 2, 1, 1 + leaf
+    auto fwarps = [&](int fuse, bool leaf) {
+        const int i = fuse == 2 ? 0 : leaf ? 2 : 1;
+        if (fused_warps[i] < 0)
+            fused_warps[i] = cc::fused_warps_per_launch(nw, (int)n, packed, fuse, leaf, sms);
+        return fused_warps[i];
+    };
     const uint32_t W = opt.shard_count;
     // Multi-GPU partition: the first frontier level with >= threshold paths is
     // split by content hash.  Deep enough that the heavy-tailed subtree sizes average out (P10x10
@@ -828,9 +843,14 @@ static cc_status enumerate_impl(const cc_graph *cg, const cc_options *opt_in, cc
     int trace_level = 0;
     // emit: the launch creates paths (children / triplets); leaf: last-level fusion (count the
     // children, write none -- cc::Scratch)
+    // fuse (EXPAND only): 0 = k_expand_blocked & co., 1 / 2 = k_expand_fused over 1 / 2 levels
+    // with output chunks of 2^log_ch slots.  On success *real_in / *real_out are the paths read and
+    // records written (the fused and blocked kernels skip and leave empty slots; the others equal
+    // n_in and the output count).
+    u64 real_in = 0, real_out = 0;
     auto launch = [&](Kind kind, const uint32_t *in, size_t n_in_pages, u64 n_in, u64 pair_lo, bool emit,
                       bool leaf, bool count, bool filter, std::vector<uint32_t> &used,
-                      bool *overflow) -> cc_status {
+                      bool *overflow, int fuse = 0, uint32_t log_ch = 0) -> cc_status {
         *overflow = false;
         const bool writes = emit && !leaf;
         const size_t nfree = free_pages.size();
@@ -865,6 +885,8 @@ static cc_status enumerate_impl(const cc_graph *cg, const cc_options *opt_in, cc
                                     kind == STAGE1 ? grid_s1 : kind == EXPAND ? grid_ex : grid_sf));
         else if (kind == STAGE1)
             CC_CUDA(cc::launch_stage1(a, mode, st, grid_s1));
+        else if (kind == EXPAND && fuse)
+            CC_CUDA(cc::launch_fused(a, fuse, leaf, log_ch, fwarps(fuse, leaf), st));
         else if (kind == EXPAND)
             CC_CUDA(cc::launch_expand(a, mode, variant, st, grid_ex));
         else
@@ -899,8 +921,11 @@ static cc_status enumerate_impl(const cc_graph *cg, const cc_options *opt_in, cc
             return CC_OK;
         }
         cyc_committed = h_sc->cyc_count;
+        const bool reports = kind == EXPAND && mode == cc::Mode::B && !wide && !list;
+        real_in = reports ? h_sc->paths_cur : n_in;
+        real_out = reports ? h_sc->out_real : h_sc->out_count;
         if (kind != FILTER)
-            S.paths_written += h_sc->out_count;
+            S.paths_written += real_out;
         const u64 npg = (h_sc->out_count + P - 1) / P;
         used.clear();
         for (u64 i = 0; i < npg; ++i) {
@@ -1016,6 +1041,8 @@ static cc_status enumerate_impl(const cc_graph *cg, const cc_options *opt_in, cc
                 res->counts[t + 1] += hy[t];
                 S.paths_expanded += hc[t];
                 S.bytes_alg += (hc[t] + hc[t + 1]) * rec_bytes;
+                S.records_levelsync += hc[t] + hc[t + 1];
+                S.slots_moved += hc[t] + hc[t + 1];
                 S.paths_written += hc[t + 1];
                 S.rounds = std::max<u64>(S.rounds, (u64)t);
             }
@@ -1065,19 +1092,32 @@ static cc_status enumerate_impl(const cc_graph *cg, const cc_options *opt_in, cc
         const bool emit = max_len == 0 || (u64)d + 1 < max_len;
         const bool leaf = emit && mode == cc::Mode::B && max_len != 0 && (u64)d + 2 >= max_len;
         const bool writes = emit && !leaf;
-        // F_{d+1} is empty here (d is the deepest non-empty level); its flags are set when this
-        // expansion commits, never before the launch (an overflow may still shard F_d first)
-        Level &C = levels[d + 1];
+        // grid class, large levels: k_expand_fused, two levels (F_d -> F_{d+2}) when the
+        // grandchildren are written (not the last level under the cap), else one
+        const int fuse = fused_ok && L.count >= fused_min ? ((max_len == 0 || (u64)d + 3 < max_len) ? 2 : 1) : 0;
+        // F_{d+1} (and F_{d+2}) are empty here (d is the deepest non-empty level); the output
+        // level's flags are set when this expansion commits, never before the launch (an
+        // overflow may still shard F_d first)
+        Level &C = levels[d + (fuse == 2 ? 2 : 1)];
+        auto est1 = [&](int t) {
+            return levels[t].fan1 > 0 ? levels[t].fan1 : (t > 3 && levels[t - 1].fan1 > 0 ? levels[t - 1].fan1 * 1.3 : maxfan);
+        };
+        const double fan_cap = fuse == 2 ? maxfan * maxfan : maxfan;
         // ---- choose the input chunk: the last k pages of F_d
         size_t k = L.pages.size();
         if (writes && (W == 1 || L.sharded)) {
-            double f = L.fan > 0 ? L.fan * 1.15 : (levels[d - 1].fan > 0 ? levels[d - 1].fan * 1.5 : maxfan);
-            f = std::min(std::max(f, 0.05), maxfan);
+            double f = L.fan > 0 && L.fan_fuse == fuse ? L.fan * 1.15
+                       : fuse == 2                   ? est1(d) * est1(d + 1) * 1.2
+                       : fuse == 1                   ? est1(d) * 1.2
+                       : (levels[d - 1].fan > 0 && levels[d - 1].fan_fuse == 0 ? levels[d - 1].fan * 1.5 : maxfan);
+            f = std::min(std::max(f, 0.05), fan_cap);
             // keep a reserve so that the child level can expand its first page next (about
             // f pages of grandchildren): without it a high fan-out level fills every free page
             // with children that then cannot be expanded
             const double reserve = (std::ceil(f * 1.2) + 1.0) * (double)P;
-            const double room = std::max((double)P, (double)free_pages.size() * P - reserve);
+            // the fused kernel may leave up to one chunk of empty slots per warp
+            const double holes = fuse ? (double)fwarps(fuse, leaf) * 1024.0 : 0.0;
+            const double room = std::max((double)P, (double)free_pages.size() * P - reserve - holes);
             // records of the last k pages: (k-1) full pages + the partial last page
             const u64 last_fill = L.count - (u64)(L.pages.size() - 1) * P;
             u64 take = (u64)std::max(1.0, room / f);
@@ -1111,7 +1151,19 @@ static cc_status enumerate_impl(const cc_graph *cg, const cc_options *opt_in, cc
             }
             bool of = false;
             trace_level = d;
-            cc_status s = launch(EXPAND, in, 1 + (sub ? 0 : k - 1), c, 0, emit, leaf, owner, false, used, &of);
+            // output chunk of the fused kernel: about 1/64 of a warp's expected output, so the
+            // empty slots at the warps' ends stay near 1% of the launch's output
+            uint32_t log_ch = 10;
+            if (fuse) {
+                const double fe = L.fan > 0 && L.fan_fuse == fuse ? L.fan : (fuse == 2 ? est1(d) * est1(d + 1) : est1(d));
+                const double warps = std::max(1.0, std::min((double)fwarps(fuse, leaf), (double)c / 32.0));
+                const double per = (double)c * fe / (warps * 64.0);
+                log_ch = 5;
+                while (log_ch < 10 && (double)(2u << log_ch) <= per && (2ull << log_ch) <= P)
+                    ++log_ch;
+            }
+            cc_status s = launch(EXPAND, in, 1 + (sub ? 0 : k - 1), c, 0, emit, leaf, owner, false, used, &of, fuse,
+                                 log_ch);
             if (tail_page != UINT32_MAX)
                 free_pages.push_back(tail_page);  // a copy: the records still live in L's last page
             if (s != CC_OK)
@@ -1129,12 +1181,14 @@ static cc_status enumerate_impl(const cc_graph *cg, const cc_options *opt_in, cc
                                                          " needs " + std::to_string(h_sc->out_count) +
                                                          " output records, " +
                                                          std::to_string(free_pages.size() * P) + " free");
-                    L.fan = std::max(L.fan, (double)h_sc->out_count / (double)c);
+                    L.fan = std::max(L.fan_fuse == fuse ? L.fan : 0.0, (double)h_sc->out_count / (double)c);
+                    L.fan_fuse = fuse;
                     const double room = (double)(free_pages.size() - 1) * P;
                     sub = std::max<u64>(1, std::min<u64>(c / 2, (u64)(room / (L.fan * 1.15))));
                     continue;
                 }
-                L.fan = std::max(L.fan, (double)h_sc->out_count / (double)c);
+                L.fan = std::max(L.fan_fuse == fuse ? L.fan : 0.0, (double)h_sc->out_count / (double)c);
+                L.fan_fuse = fuse;
                 const double room = (double)free_pages.size() * P;
                 const double want = room / (L.fan * 1.15);
                 size_t k2 = want <= last_fill ? 1 : 1 + (size_t)((want - last_fill) / P);
@@ -1145,22 +1199,35 @@ static cc_status enumerate_impl(const cc_graph *cg, const cc_options *opt_in, cc
             S.chunks++;
             S.rounds = std::max<u64>(S.rounds, (u64)d);
             if (owner) {
-                res->paths[d] += c;
+                res->paths[d] += real_in;
                 res->cand[d] += h_sc->cand;
-                S.paths_expanded += c;
+                S.paths_expanded += real_in;
                 res->counts[d + 1] += h_sc->cycles;
                 res->hash += h_sc->hash;
-                if (leaf) {  // the children: counted here, never written
+                if (leaf || fuse == 2) {  // the children: counted here, never written
                     res->paths[d + 1] += h_sc->paths_next;
                     res->cand[d + 1] += h_sc->cand_next;
                     res->counts[d + 2] += h_sc->cycles_next;
                     S.paths_expanded += h_sc->paths_next;
-                    S.leaf_paths += h_sc->paths_next;
+                    if (leaf)
+                        S.leaf_paths += h_sc->paths_next;
                 }
             }
-            S.bytes_alg += (c + h_sc->out_count) * rec_bytes;
-            if (c > 0)
+            // records actually read + written (empty slots excluded), and what a level-synchronous
+            // expansion of the same paths reads + writes (each path read once, each
+            // child written once; the fused kernel keeps F_{d+1} in shared memory)
+            S.bytes_alg += (real_in + real_out) * rec_bytes;
+            S.records_levelsync += real_in + real_out + ((leaf || fuse == 2) ? 2 * h_sc->paths_next : 0);
+            S.slots_moved += c + h_sc->out_count;
+            if (c > 0) {
                 L.fan = (double)h_sc->out_count / (double)c;
+                L.fan_fuse = fuse;
+            }
+            if (real_in > 0 && mode == cc::Mode::B && !wide && !list) {
+                L.fan1 = (double)(fuse == 2 || leaf ? h_sc->paths_next : real_out) / (double)real_in;
+                if (fuse == 2 && h_sc->paths_next > 0)
+                    levels[d + 1].fan1 = (double)real_out / (double)h_sc->paths_next;
+            }
             if (!sub)
                 for (size_t i = 0; i < k; ++i) {
                     free_pages.push_back(L.pages.back());
@@ -1175,7 +1242,7 @@ static cc_status enumerate_impl(const cc_graph *cg, const cc_options *opt_in, cc
                 C.shard_now = false;
                 in_use += C.count;
                 high_water = std::max(high_water, in_use);
-                deepest = d + 1;
+                deepest = d + (fuse == 2 ? 2 : 1);
             }
             break;
         }

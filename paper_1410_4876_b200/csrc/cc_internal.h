@@ -90,6 +90,9 @@ struct Scratch {
     u64 cycles_next;             // last-level fusion: closures of the children (t+2 vertices)
     u64 cand_next;               // last-level fusion: candidate slots of the children
     u64 paths_next;              // last-level fusion: children counted (|F_{t+1}| share)
+    u64 paths_cur;               // real input paths expanded (k_expand_blocked / k_expand_fused: the
+                                 // input may hold empty slots, DESIGN.md §5 "output chunks")
+    u64 out_real;                // real records written (out_count also counts empty slots)
     u64 cyc_count;               // collect-mode store counter (NOT reset per launch)
 };
 
@@ -165,6 +168,12 @@ cudaError_t launch_cycle_lengths(const CycleStore &c, int nw, uint64_t first, ui
 cudaError_t launch_cycle_sequences(const CycleStore &c, int nw, const u64 *adj, const int32_t *orig,
                                    uint64_t first, uint64_t count, const u64 *offsets,
                                    int32_t *out, cudaStream_t st);
+// Two-level (fuse = 2) or single-level (fuse = 1, optionally last-level fusion) expansion for the
+// grid class: count mode, B-mode records, nw <= 2, max degree <= 4 (cc_fused.cu).  Output slots
+// come in per-warp chunks of 2^log_ch; unused slots are all-zero records (v1 == v2).
+cudaError_t launch_fused(const LaunchArgs &a, int fuse, bool leaf, uint32_t log_ch, int max_warps, cudaStream_t st);
+int fused_warps_per_launch(int nw, int n, bool packed, int fuse, bool leaf, int sms);
+size_t fused_smem(int nw, int n, bool packed, int fuse);
 // dynamic shared memory of the expansion kernel for (mode, nw, n, packed)
 size_t expand_smem(Mode m, int nw, int n, bool packed);
 // Wide class (512 < n <= 2015, count mode, AoS records): which 0 = Stage 1, 1 = expand,

@@ -507,3 +507,53 @@ def test_max_len_below_three_counts_nothing(ws, K):
     want = oracle.enumerate_cycles(*g, max_len=K)
     assert int(got["counts"].sum()) == 0 == int(want["counts"].sum())
     assert_same(got, want)
+
+
+FUSED_GRAPHS = [("grid5x6", I.grid(5, 6), 0), ("grid6x7", I.grid(6, 7), 0), ("grid7x8", I.grid(7, 8), 0),
+                ("grid7x10_k14", I.grid(7, 10), 14), ("grid7x10_k15", I.grid(7, 10), 15),
+                ("grid6x10_k9", I.grid(6, 10), 9), ("p8x3", I.grid(8, 3), 0), ("c40", I.cycle(40), 0),
+                ("grid6x6_k5", I.grid(6, 6), 5), ("grid6x6_k4", I.grid(6, 6), 4)]
+
+
+@pytest.mark.parametrize("name,g,K", FUSED_GRAPHS, ids=[x[0] for x in FUSED_GRAPHS])
+def test_fused_two_level_kernel_every_level(ws, name, g, K):
+    """k_expand_fused (grid class, DESIGN.md §2 step 3d) on every level (CC_FUSED_MIN=1): two
+    levels per launch, output chunks with empty slots, single-level and last-level-fusion
+    launches near the cap.  Counts, hash, |F_t| and candidates equal the oracle's; the empty
+    slots never count."""
+    want = oracle.enumerate_cycles(*g, max_len=K, nthreads=NT)
+    os.environ["CC_FUSED_MIN"] = "1"
+    os.environ["CC_NO_SMALL"] = "1"
+    try:
+        got = gpu(g, ws, max_len=K)
+    finally:
+        del os.environ["CC_FUSED_MIN"]
+        del os.environ["CC_NO_SMALL"]
+    assert_same(got, want)
+    s = got["stats"]
+    f = got["paths_by_len"]
+    # every level but the fused intermediates is written; levelsync counts each once read/written
+    assert s["paths_expanded"] == int(f.sum())
+    assert s["slots_moved"] >= s["bytes_alg"] // s["record_bytes"]
+
+
+@pytest.mark.parametrize("kb", [256, 1024])
+def test_fused_kernel_small_arena_chunks(ws, kb):
+    """The fused kernel under the deepest-first chunk scheduler: a P7xP8 arena of 256 KB / 1 MB
+    forces chunked, retried (overflowing) launches and sub-page chunks; results unchanged."""
+    import torch
+    g = I.grid(7, 8)
+    small = torch.empty(kb * 1024, dtype=torch.uint8, device="cuda")
+    os.environ["CC_FUSED_MIN"] = "1"
+    try:
+        got = binding.enumerate_cycles(*g, workspace=small)
+        parts = [binding.enumerate_cycles(*g, workspace=small, shard_index=i, shard_count=2, min_shard_paths=64)
+                 for i in range(2)]
+    finally:
+        del os.environ["CC_FUSED_MIN"]
+    want = oracle.enumerate_cycles(*g, nthreads=NT)
+    assert_same(got, want)
+    assert got["stats"]["chunks"] > got["stats"]["rounds"] // 2
+    assert sum(p["counts"] for p in parts).tolist() == want["counts"].tolist()
+    assert sum(p["set_hash"] for p in parts) % (1 << 64) == want["set_hash"]
+    assert sum(p["paths_by_len"] for p in parts).tolist() == want["paths_by_len"].tolist()

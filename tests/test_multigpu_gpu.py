@@ -36,7 +36,9 @@ def _worker(rank, world, port, graph_name, max_len, ws_bytes, out_q):
     torch.cuda.set_device(0)
     ws = torch.empty(ws_bytes, dtype=torch.uint8, device="cuda:0")
     g = inputs.named(graph_name)
-    r = binding.enumerate_cycles(*g, workspace=ws, max_len=max_len, shard_index=rank, shard_count=world)
+    # min_shard_paths 2^16: P8x8 (peak level 2.9e6 paths) is split at every W tested
+    r = binding.enumerate_cycles(*g, workspace=ws, max_len=max_len, shard_index=rank, shard_count=world,
+                                 min_shard_paths=1 << 16)
     counts, h, paths = D.combine_shards(r["counts"], r["set_hash"], int(r["paths_by_len"].sum()))
     _, _, cand = D.combine_shards(r["counts"][:1] * 0, 0, int(r["candidates"]))
     mine = int(r["paths_by_len"].sum())
