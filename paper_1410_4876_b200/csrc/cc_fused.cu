@@ -35,13 +35,13 @@ constexpr int kFCh2 = kFCh1 * kFMaxCh;   // grandchildren of one warp tile
 
 template <int NW, bool PACK, int FUSE>
 struct FusedWarpSmem {
-    static constexpr int PW = 2 * NW + 1;               // B | N[vt] (NW), keysum, Ext (NW)
+    static constexpr int PW = NW + 1;                   // B | N[vt] (v1, v2 packed), keysum
     u64 par[32][PW];                                    // level-t parents with children
     u64 par2[FUSE == 2 ? kFCh1 : 1][PW];                // level-(t+1) children with children
     uint32_t pid[PACK ? 1 : 32];                        // unpacked ids: v1 | v2 << 10
     uint32_t pid2[(PACK || FUSE == 1) ? 1 : kFCh1];
-    uint8_t ent1[kFCh1];                                // child k: parent lane | rank << 5
-    uint16_t ent2[FUSE == 2 ? kFCh2 : 1];               // grandchild k: child index | rank << 7
+    uint16_t ent1[kFCh1];                               // child: parent lane | v << 5
+    uint16_t ent2[FUSE == 2 ? kFCh2 : 1];               // grandchild: child index | w << 7
 };
 
 template <int NW, bool PACK, int FUSE>
@@ -50,79 +50,78 @@ __host__ __device__ constexpr size_t fused_warp_bytes()
     return (sizeof(FusedWarpSmem<NW, PACK, FUSE>) + 15) & ~(size_t)15;
 }
 
-// rank-th (rank < 3) set bit of the NW-word set x
+// remove and return the lowest element of the NW-word set x (x != 0)
 template <int NW>
-__device__ __forceinline__ uint32_t select_bit(const u64 (&x)[NW], uint32_t rank)
+__device__ __forceinline__ uint32_t pop_lowest(u64 (&x)[NW])
 {
-    u64 w = x[0];
-    uint32_t wsel = 0;
-#pragma unroll
-    for (int i = 1; i < NW; ++i) {
-        const uint32_t pc = __popcll(w);
-        const bool next = rank >= pc;
-        rank = next ? rank - pc : rank;
-        wsel = next ? (uint32_t)i : wsel;
-        w = next ? x[i] : w;
+    if constexpr (NW == 1) {
+        const uint32_t b = (uint32_t)__ffsll((long long)x[0]) - 1;
+        x[0] &= x[0] - 1;
+        return b;
+    } else {
+        const bool lo = x[0] != 0ull;
+        u64 w = lo ? x[0] : x[1];
+        const uint32_t b = (uint32_t)__ffsll((long long)w) - 1 + (lo ? 0u : 64u);
+        w &= w - 1;
+        x[0] = lo ? w : x[0];
+        x[1] = lo ? x[1] : w;
+        return b;
     }
-#pragma unroll
-    for (int c = 1; c < kFMaxCh; ++c) {
-        const u64 y = w & (w - 1);
-        w = (uint32_t)c <= rank ? y : w;
-    }
-    return 64 * wsel + (uint32_t)__ffsll((long long)w) - 1;
 }
 
-// Per-warp output cursor over chunks of 2^log_ch slots (warp-uniform state).
+// Per-warp output cursor (warp-uniform): the current chunk of 2^log_ch slots.  log_ch is at
+// least the largest single reservation (kFCh2 grandchildren), so a reservation never needs more
+// than one new chunk, and a chunk (chunk-aligned, 2^log_ch <= page) never straddles a page.
 struct WarpOut {
-    u64 pos = 0;          // next free slot of the current chunk
-    uint32_t left = 0;    // free slots left in it
+    char *pp = nullptr;   // page of the current chunk
+    uint32_t slot = 0;    // next free slot in that page
+    uint32_t left = 0;    // free slots left in the chunk
     bool dead = false;    // output overflow: the launch is discarded by the host
 };
 
-// Reserve T slots (warp-uniform T): slots k < split are pos0 + k, the others pos1 + (k - split).
+// Reserve T <= 2^log_ch slots: slot k < split is (pp0, s0 + k), the others (pp1, s1 + k - split).
 __device__ __forceinline__ void warp_reserve(WarpOut &o, uint32_t T, uint32_t log_ch, const LaunchArgs &p,
-                                             u64 &pos0, u64 &pos1, uint32_t &split)
+                                             char *&pp0, uint32_t &s0, char *&pp1, uint32_t &s1, uint32_t &split)
 {
-    pos0 = o.pos;
-    pos1 = 0;
+    pp0 = pp1 = o.pp;
+    s0 = s1 = o.slot;
     split = T;
     if (T <= o.left) {
-        o.pos += T;
+        o.slot += T;
         o.left -= T;
         return;
     }
-    const uint32_t need = T - o.left;
-    const u64 nch = ((u64)need + (1u << log_ch) - 1) >> log_ch;
     u64 nb = 0;
     if ((threadIdx.x & 31) == 0)
-        nb = atomicAdd(&p.sc->out_count, nch << log_ch);
+        nb = atomicAdd(&p.sc->out_count, 1ull << log_ch);
     nb = __shfl_sync(FULL_MASK, nb, 0);
-    if (nb + (nch << log_ch) > p.out_cap) {
+    if (nb + (1ull << log_ch) > p.out_cap) {
         if ((threadIdx.x & 31) == 0)
             p.sc->err = 1;
         o.dead = true;
         o.left = 0;
         return;
     }
+    const u64 vo = p.out_off + nb;
     split = o.left;
-    pos1 = nb;
-    o.pos = nb + need;
-    o.left = (uint32_t)((nch << log_ch) - need);
+    pp1 = page_ptr(p.pg, p.pg.out_pages[vo >> p.pg.log_p]);
+    s1 = (uint32_t)(vo & ((1ull << p.pg.log_p) - 1));
+    const uint32_t need = T - o.left;
+    o.pp = pp1;
+    o.slot = s1 + need;
+    o.left = (1u << log_ch) - need;
 }
 
-// store record C (RW words, plus the ids word when unpacked) at virtual output position o
+// store record C (RW words, plus the ids word when unpacked) at `slot` of page pp
 template <int RW, bool PACK>
-__device__ __forceinline__ void put_record(const LaunchArgs &p, u64 o, const u64 (&C)[RW], uint32_t id)
+__device__ __forceinline__ void put_record(char *pp, uint32_t slot, uint32_t log_p, const u64 (&C)[RW], uint32_t id)
 {
-    o += p.out_off;
-    char *pp = page_ptr(p.pg, p.pg.out_pages[o >> p.pg.log_p]);
-    const u64 slot = o & ((1ull << p.pg.log_p) - 1);
     u64 *w0 = (u64 *)pp + slot;
 #pragma unroll
     for (int w = 0; w < RW; ++w)
-        w0[(u64)w << p.pg.log_p] = C[w];
+        w0[(u64)w << log_p] = C[w];
     if (!PACK)
-        ((uint32_t *)(pp + ((u64)RW << p.pg.log_p) * 8))[slot] = id;
+        ((uint32_t *)(pp + ((u64)RW << log_p) * 8))[slot] = id;
 }
 
 template <int NW, bool PACK, int FUSE, bool LEAF>
@@ -131,6 +130,11 @@ __global__ void __launch_bounds__(kFBlock, 4) k_expand_fused(const LaunchArgs p,
     static_assert(FUSE == 1 || !LEAF, "last-level fusion is single-level");
     constexpr int RW = NW + 1;
     using WS = FusedWarpSmem<NW, PACK, FUSE>;
+    // packed ids: a fixed width per word count (the host packs with the same, cc_host.cpp)
+    constexpr uint32_t IDB = PACK ? 5 + NW : (uint32_t)kIdBits;
+    constexpr uint32_t IDM = (1u << IDB) - 1;
+    constexpr uint32_t V12M = (1u << (2 * IDB)) - 1;
+    constexpr u64 KEEP_V12 = PACK ? ~((u64)IDM << (64 - IDB)) : ~0ull;  // packed: clears the vt field
     extern __shared__ __align__(16) u64 smem[];
     const int n = p.g.n;
     u64 *s_adj = smem;                          // closed rows N[v] = Adj(v) | {v}
@@ -147,12 +151,7 @@ __global__ void __launch_bounds__(kFBlock, 4) k_expand_fused(const LaunchArgs p,
     __syncthreads();
 
     const int lane = threadIdx.x & 31;
-    const uint32_t idb = PACK ? p.idb : (uint32_t)kIdBits;
-    const uint32_t idm = (1u << idb) - 1;
-    const uint32_t v12m = (1u << (2 * idb)) - 1;
-    const u64 keep_v12 = PACK ? ~((u64)idm << (64 - idb)) : ~0ull;  // packed: clears the vt field
-    const u64 P = 1ull << p.pg.log_p;
-    const u64 pmask = P - 1;
+    const uint32_t log_p = p.pg.log_p;
     const u64 nt = (p.n_in + 31) >> 5;
     const u64 tw = (u64)gridDim.x * kFWarps;
     WarpOut out;
@@ -162,55 +161,51 @@ __global__ void __launch_bounds__(kFBlock, 4) k_expand_fused(const LaunchArgs p,
 
     auto load = [&](u64 wt, u64 (&X)[RW], uint32_t &xid) {
         const u64 r0 = wt << 5;
-        const char *pp = page_ptr(p.pg, p.pg.in_pages[r0 >> p.pg.log_p]);
-        const u64 slot = (r0 & pmask) + lane;
+        const char *pp = page_ptr(p.pg, p.pg.in_pages[r0 >> log_p]);
+        const uint32_t slot = (uint32_t)(r0 & ((1ull << log_p) - 1)) + lane;
 #pragma unroll
         for (int w = 0; w < RW; ++w)
-            X[w] = __ldcs((const u64 *)pp + ((u64)w << p.pg.log_p) + slot);  // read once: evict first
-        xid = PACK ? 0u : __ldcs((const uint32_t *)(pp + ((u64)RW << p.pg.log_p) * 8) + slot);
+            X[w] = __ldcs((const u64 *)pp + ((u64)w << log_p) + slot);  // read once: evict first
+        xid = PACK ? 0u : __ldcs((const uint32_t *)(pp + ((u64)RW << log_p) * 8) + slot);
     };
-    // copy T staged records to the warp's output slots (uniform loop, consecutive slots)
+    // copy T staged records to consecutive output slots (uniform loop)
     auto emit = [&](uint32_t T, bool second) {
         if (T == 0 || out.dead)
             return;
-        u64 pos0, pos1;
-        uint32_t split;
-        warp_reserve(out, T, log_ch, p, pos0, pos1, split);
+        char *pp0, *pp1;
+        uint32_t s0, s1, split;
+        warp_reserve(out, T, log_ch, p, pp0, s0, pp1, s1, split);
         if (out.dead)
             return;
-        written += T;  // counted once per warp below (lane 0 share)
+        written += T;  // every lane adds the warp's total; lane 0's copy is flushed
         for (uint32_t k = lane; k < T; k += 32) {
-            uint32_t q, rank;
+            uint32_t e, q, v;
             const u64 *par;
             uint32_t pid = 0;
             if (FUSE == 2 && second) {
-                const uint32_t e = ws.ent2[k];
+                e = ws.ent2[k];
                 q = e & 127;
-                rank = e >> 7;
+                v = e >> 7;
                 par = ws.par2[q];
                 if (!PACK)
                     pid = ws.pid2[q];
             } else {
-                const uint32_t e = ws.ent1[k];
+                e = ws.ent1[k];
                 q = e & 31;
-                rank = e >> 5;
+                v = e >> 5;
                 par = ws.par[q];
                 if (!PACK)
                     pid = ws.pid[q];
             }
-            u64 ex[NW];
-#pragma unroll
-            for (int w = 0; w < NW; ++w)
-                ex[w] = par[NW + 1 + w];
-            const uint32_t v = select_bit<NW>(ex, rank);
             u64 C[RW];
 #pragma unroll
             for (int w = 0; w < NW; ++w)
                 C[w] = par[w];
             C[NW] = par[NW] + s_key[v];
             if (PACK)
-                C[NW - 1] |= (u64)v << (64 - idb);
-            put_record<RW, PACK>(p, k < split ? pos0 + k : pos1 + (k - split), C, pid | (v << (2 * idb)));
+                C[NW - 1] |= (u64)v << (64 - IDB);
+            const bool lo = k < split;
+            put_record<RW, PACK>(lo ? pp0 : pp1, lo ? s0 + k : s1 + (k - split), log_p, C, pid | (v << (2 * IDB)));
         }
     };
 
@@ -226,8 +221,8 @@ __global__ void __launch_bounds__(kFBlock, 4) k_expand_fused(const LaunchArgs p,
             load(wt + tw, Wn, idn);
         // ---------------------------------------------------------------- level t
         const u64 r = (wt << 5) + lane;
-        const uint32_t ids = PACK ? (uint32_t)packed_ids(W[NW - 1], idb) : id;
-        const uint32_t v1 = ids & idm, v2 = (ids >> idb) & idm, vt = ids >> (2 * idb);
+        const uint32_t ids = PACK ? (uint32_t)(W[NW - 1] >> (64 - 3 * IDB)) : id;
+        const uint32_t v1 = ids & IDM, v2 = (ids >> IDB) & IDM, vt = ids >> (2 * IDB);
         const bool valid = r < p.n_in && v1 != v2;  // v1 == v2: an empty slot
         u64 ext[NW];
         uint32_t nc = 0;
@@ -305,20 +300,17 @@ __global__ void __launch_bounds__(kFBlock, 4) k_expand_fused(const LaunchArgs p,
                 for (int w = 0; w < NW; ++w)
                     nc += __popcll(ext[w]);
                 if (nc) {
-                    // stage the parent: B | N[vt] (vt field cleared), keysum, Ext
+                    // stage the parent: B | N[vt] (vt field cleared), keysum
 #pragma unroll
                     for (int w = 0; w < NW; ++w)
-                        ws.par[lane][w] = (W[w] | arow[w]) & (w == NW - 1 ? keep_v12 : ~0ull);
+                        ws.par[lane][w] = (W[w] | arow[w]) & (w == NW - 1 ? KEEP_V12 : ~0ull);
                     ws.par[lane][NW] = W[NW];
-#pragma unroll
-                    for (int w = 0; w < NW; ++w)
-                        ws.par[lane][NW + 1 + w] = ext[w];
                     if (!PACK)
-                        ws.pid[lane] = ids & v12m;
+                        ws.pid[lane] = ids & V12M;
                 }
             }
         }
-        // warp scan of the child counts -> each child's slot in ent1
+        // warp scan of the child counts -> each child's entry (parent lane, vertex)
         uint32_t incl = nc;
 #pragma unroll
         for (int o = 1; o < 32; o <<= 1) {
@@ -332,40 +324,37 @@ __global__ void __launch_bounds__(kFBlock, 4) k_expand_fused(const LaunchArgs p,
 #pragma unroll
             for (uint32_t c = 0; c < (uint32_t)kFMaxCh; ++c)
                 if (c < nc)
-                    ws.ent1[off + c] = (uint8_t)(lane | (c << 5));
+                    ws.ent1[off + c] = (uint16_t)(lane | (pop_lowest<NW>(ext) << 5));
         }
         __syncwarp();
         if constexpr (FUSE == 1) {
             emit(T1, false);
         } else {
             // ------------------------------------------------------------ level t+1 (in smem)
-            uint32_t ng[kFMaxCh];
+            uint32_t base2 = 0;
+            for (uint32_t b = 0; b < T1; b += 32) {  // warp-uniform rounds of 32 children
+                const uint32_t j = b + lane;
+                uint32_t g = 0;
+                u64 ex2[NW];
 #pragma unroll
-            for (int ro = 0; ro < kFMaxCh; ++ro) {
-                ng[ro] = 0;
-                const uint32_t j = 32 * ro + lane;
-                if (32 * (uint32_t)ro >= T1)
-                    continue;  // warp-uniform
+                for (int w = 0; w < NW; ++w)
+                    ex2[w] = 0;
                 if (j < T1) {
                     const uint32_t e = ws.ent1[j];
-                    const uint32_t q = e & 31;
-                    u64 Bc[NW], ex[NW];
+                    const uint32_t q = e & 31, v = e >> 5;
+                    u64 Bc[NW];
 #pragma unroll
-                    for (int w = 0; w < NW; ++w) {
+                    for (int w = 0; w < NW; ++w)
                         Bc[w] = ws.par[q][w];
-                        ex[w] = ws.par[q][NW + 1 + w];
-                    }
-                    const uint32_t v = select_bit<NW>(ex, e >> 5);
                     const u64 ksc = ws.par[q][NW] + s_key[v];
-                    const uint32_t cid = PACK ? (uint32_t)packed_ids(Bc[NW - 1], idb) : ws.pid[q];
-                    const uint32_t c1 = cid & idm, c2 = (cid >> idb) & idm;
+                    const uint32_t cid = PACK ? (uint32_t)(Bc[NW - 1] >> (64 - 3 * IDB)) : ws.pid[q];
+                    const uint32_t c1 = cid & IDM, c2 = (cid >> IDB) & IDM;
                     n_next++;
-                    u64 arow[NW], abv[NW], a1[NW], ex2[NW];
+                    u64 arow[NW], abv[NW], a1[NW];
                     lds_row<NW>(s_adj, v, arow);
                     lds_row<NW>(s_above, c2, abv);
                     lds_row<NW>(s_adj, c1, a1);
                     cand2 -= 1;
-                    uint32_t g = 0;
 #pragma unroll
                     for (int w = 0; w < NW; ++w) {
                         cand2 += __popcll(arow[w]);
@@ -376,48 +365,37 @@ __global__ void __launch_bounds__(kFBlock, 4) k_expand_fused(const LaunchArgs p,
                         if (p.count) {
                             cnt2 += __popcll(cl);
                             while (cl) {
-                                const int b = __ffsll((long long)cl) - 1;
+                                const int bb = __ffsll((long long)cl) - 1;
                                 cl &= cl - 1;
-                                hs += mix64(ksc + s_key[64 * w + b]);
+                                hs += mix64(ksc + s_key[64 * w + bb]);
                             }
                         }
                     }
-                    ng[ro] = g;
                     if (g) {
 #pragma unroll
                         for (int w = 0; w < NW; ++w)
                             ws.par2[j][w] = Bc[w] | arow[w];  // v1, v2 stay in the packed bits
                         ws.par2[j][NW] = ksc;
-#pragma unroll
-                        for (int w = 0; w < NW; ++w)
-                            ws.par2[j][NW + 1 + w] = ex2[w];
                         if (!PACK)
                             ws.pid2[j] = cid;
                     }
                 }
-            }
-            // lane L owns children L, L+32, L+64: one contiguous block of grandchild slots
-            const uint32_t mine = ng[0] + ng[1] + ng[2];
-            uint32_t inc2 = mine;
+                uint32_t inc2 = g;
 #pragma unroll
-            for (int o = 1; o < 32; o <<= 1) {
-                const uint32_t x = __shfl_up_sync(FULL_MASK, inc2, o);
-                if (lane >= o)
-                    inc2 += x;
-            }
-            const uint32_t T2 = __shfl_sync(FULL_MASK, inc2, 31);
-            uint32_t off = inc2 - mine;
-#pragma unroll
-            for (int ro = 0; ro < kFMaxCh; ++ro) {
-                const uint32_t j = 32 * ro + lane;
+                for (int o = 1; o < 32; o <<= 1) {
+                    const uint32_t x = __shfl_up_sync(FULL_MASK, inc2, o);
+                    if (lane >= o)
+                        inc2 += x;
+                }
+                const uint32_t off2 = base2 + inc2 - g;
 #pragma unroll
                 for (uint32_t c = 0; c < (uint32_t)kFMaxCh; ++c)
-                    if (c < ng[ro])
-                        ws.ent2[off + c] = (uint16_t)(j | (c << 7));
-                off += ng[ro];
+                    if (c < g)
+                        ws.ent2[off2 + c] = (uint16_t)(j | (pop_lowest<NW>(ex2) << 7));
+                base2 += __shfl_sync(FULL_MASK, inc2, 31);
             }
             __syncwarp();
-            emit(T2, true);
+            emit(base2, true);
         }
         __syncwarp();  // the next tile overwrites par / ent
 #pragma unroll
@@ -432,7 +410,7 @@ __global__ void __launch_bounds__(kFBlock, 4) k_expand_fused(const LaunchArgs p,
         for (int w = 0; w < RW; ++w)
             Z[w] = 0;
         for (uint32_t k = lane; k < out.left; k += 32)
-            put_record<RW, PACK>(p, out.pos + k, Z, 0u);
+            put_record<RW, PACK>(out.pp, out.slot + k, log_p, Z, 0u);
     }
     if (!p.count) {
         cand1 = cand2 = 0;
@@ -494,7 +472,7 @@ int fused_warps_per_launch(int nw, int n, bool packed, int fuse, bool leaf, int 
 cudaError_t launch_fused(const LaunchArgs &a, int fuse, bool leaf, uint32_t log_ch, int max_warps, cudaStream_t st)
 {
     FusedFn f = fused_kernel(a.g.nw, a.packed != 0, fuse, leaf);
-    if (!f || a.g.n > 128 || log_ch < 5 || max_warps < kFWarps)
+    if (!f || a.g.n > 128 || (1 << log_ch) < kFCh2 || (a.pg.log_p < log_ch) || max_warps < kFWarps)
         return cudaErrorInvalidValue;
     const size_t smem = fused_smem(a.g.nw, a.g.n, a.packed != 0, fuse);
     cudaError_t e = cudaFuncSetAttribute((const void *)f, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);

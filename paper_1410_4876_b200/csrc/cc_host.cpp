@@ -761,7 +761,9 @@ static cc_status enumerate_impl(const cc_graph *cg, const cc_options *opt_in, cc
     base.root_offset = opt.root_offset;
     base.shard_index = opt.shard_index;
     base.shard_count = opt.shard_count;
-    base.idb = (uint32_t)cc::id_bits((int)n);
+    // packed bitset records: a fixed id width per word count (6 bits for NW = 1, 7 for NW = 2; the
+    // packable graphs are the same as with ceil(log2 n)), so the kernels see it as a constant
+    base.idb = (uint32_t)(packed && !wide && nw <= 2 ? 5 + nw : cc::id_bits((int)n));
     base.packed = packed ? 1 : 0;
 
     const cc::ExpandVariant variant = (mode == cc::Mode::B && g->max_deg <= 4) ? cc::ExpandVariant::Small
@@ -783,7 +785,7 @@ static cc_status enumerate_impl(const cc_graph *cg, const cc_options *opt_in, cc
     const bool fused_ok = mode == cc::Mode::B && !wide && !list && nw <= 2 && n <= 128 && g->max_deg <= 4 &&
                           std::getenv("CC_NO_FUSED") == nullptr;
     const u64 fused_min = std::getenv("CC_FUSED_MIN") ? std::strtoull(std::getenv("CC_FUSED_MIN"), nullptr, 10)
-                                                       : (1ull << 20);
+                                                       : (1ull << 24);
     int fused_warps[3] = {-1, -1, -1};  // resident warps of the fused kernel: fuse 2, 1, 1 + leaf
     auto fwarps = [&](int fuse, bool leaf) {
         const int i = fuse == 2 ? 0 : leaf ? 2 : 1;
@@ -886,7 +888,11 @@ static cc_status enumerate_impl(const cc_graph *cg, const cc_options *opt_in, cc
         else if (kind == STAGE1)
             CC_CUDA(cc::launch_stage1(a, mode, st, grid_s1));
         else if (kind == EXPAND && fuse)
-            CC_CUDA(cc::launch_fused(a, fuse, leaf, log_ch, fwarps(fuse, leaf), st));
+        {
+            // no more warps than a quarter of the free output in chunks (small arenas)
+            const u64 cap_warps = std::max<u64>(8, a.out_cap / (4ull << log_ch));
+            CC_CUDA(cc::launch_fused(a, fuse, leaf, log_ch, (int)std::min<u64>((u64)fwarps(fuse, leaf), cap_warps), st));
+        }
         else if (kind == EXPAND)
             CC_CUDA(cc::launch_expand(a, mode, variant, st, grid_ex));
         else
@@ -1116,7 +1122,7 @@ static cc_status enumerate_impl(const cc_graph *cg, const cc_options *opt_in, cc
             // with children that then cannot be expanded
             const double reserve = (std::ceil(f * 1.2) + 1.0) * (double)P;
             // the fused kernel may leave up to one chunk of empty slots per warp
-            const double holes = fuse ? (double)fwarps(fuse, leaf) * 1024.0 : 0.0;
+            const double holes = fuse ? (double)fwarps(fuse, leaf) * 4096.0 : 0.0;
             const double room = std::max((double)P, (double)free_pages.size() * P - reserve - holes);
             // records of the last k pages: (k-1) full pages + the partial last page
             const u64 last_fill = L.count - (u64)(L.pages.size() - 1) * P;
@@ -1151,15 +1157,15 @@ static cc_status enumerate_impl(const cc_graph *cg, const cc_options *opt_in, cc
             }
             bool of = false;
             trace_level = d;
-            // output chunk of the fused kernel: about 1/64 of a warp's expected output, so the
-            // empty slots at the warps' ends stay near 1% of the launch's output
-            uint32_t log_ch = 10;
+            // output chunk of the fused kernel: about 1/64 of a warp's expected output (at least
+            // 512 slots, the largest single reservation, at most 4096), so the empty slots at
+            // the warps' ends stay near 1% of the launch's output
+            uint32_t log_ch = 9;
             if (fuse) {
                 const double fe = L.fan > 0 && L.fan_fuse == fuse ? L.fan : (fuse == 2 ? est1(d) * est1(d + 1) : est1(d));
                 const double warps = std::max(1.0, std::min((double)fwarps(fuse, leaf), (double)c / 32.0));
                 const double per = (double)c * fe / (warps * 64.0);
-                log_ch = 5;
-                while (log_ch < 10 && (double)(2u << log_ch) <= per && (2ull << log_ch) <= P)
+                while (log_ch < 12 && (double)(2u << log_ch) <= per && (2ull << log_ch) <= P)
                     ++log_ch;
             }
             cc_status s = launch(EXPAND, in, 1 + (sub ? 0 : k - 1), c, 0, emit, leaf, owner, false, used, &of, fuse,

@@ -895,7 +895,9 @@ cudaError_t launch_small(const LaunchArgs &a, const SmallArgs &s, cudaStream_t s
 }
 
 // ---------------------------------------------------------------------------- shard filter
-template <int RW, bool IDS>
+// HOLES: bitset records (ids v1 | v2 | vt in the ids array or packed in word RW-2), whose levels
+// may hold empty slots; false for the list class (its words hold 16-bit vertex lists)
+template <int RW, bool IDS, bool HOLES = true>
 __global__ void __launch_bounds__(kBlock) k_shard_filter(const LaunchArgs p)
 {
     __shared__ ReserveSmem rs;
@@ -911,7 +913,8 @@ __global__ void __launch_bounds__(kBlock) k_shard_filter(const LaunchArgs p)
             // empty output-chunk slots (all-zero records, v1 == v2) are dropped here
             const uint32_t ids = IDS ? id : (uint32_t)packed_ids(W[RW - 2], p.idb);
             const uint32_t ib = IDS ? (uint32_t)kIdBits : p.idb, im = (1u << ib) - 1;
-            keep = (ids & im) != ((ids >> ib) & im) && (shard_hash<RW>(W, id) % p.shard_count) == p.shard_index;
+            keep = (!HOLES || (ids & im) != ((ids >> ib) & im)) &&
+                   (shard_hash<RW>(W, id) % p.shard_count) == p.shard_index;
         }
         const u64 off = block_reserve(keep, &p.sc->out_count, rs);
         if (keep) {
@@ -1915,7 +1918,7 @@ static KernelFn list_kernel(int which, int rwl, bool leaf)
             return leaf ? k_expand_list<3, true> : k_expand_list<3, false>;
         return nullptr;
     }
-    return rwl == 2 ? k_shard_filter<4, false> : rwl == 3 ? k_shard_filter<5, false> : nullptr;
+    return rwl == 2 ? k_shard_filter<4, false, false> : rwl == 3 ? k_shard_filter<5, false, false> : nullptr;
 }
 
 cudaError_t launch_list(int which, const LaunchArgs &a, int rwl, bool leaf, cudaStream_t st, int grid_cap)

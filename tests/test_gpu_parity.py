@@ -537,9 +537,9 @@ def test_fused_two_level_kernel_every_level(ws, name, g, K):
     assert s["slots_moved"] >= s["bytes_alg"] // s["record_bytes"]
 
 
-@pytest.mark.parametrize("kb", [256, 1024])
+@pytest.mark.parametrize("kb", [1024, 4096])
 def test_fused_kernel_small_arena_chunks(ws, kb):
-    """The fused kernel under the deepest-first chunk scheduler: a P7xP8 arena of 256 KB / 1 MB
+    """The fused kernel under the deepest-first chunk scheduler: a P7xP8 arena of 1 MB / 4 MB
     forces chunked, retried (overflowing) launches and sub-page chunks; results unchanged."""
     import torch
     g = I.grid(7, 8)
