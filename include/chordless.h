@@ -199,6 +199,9 @@ cc_status cc_paths_by_length(const cc_result *r, uint64_t *paths, size_t cap, si
  * entries).  *n_fetched = cycles written.  CC_ERR_NOT_COLLECTED on a count-only result;
  * CC_ERR_BUFFER_TOO_SMALL if vertices_cap is too small (offsets are then filled for the
  * cycles requested and *n_fetched = 0 so the caller can size the buffer).
+ * Runs on the stream the result was enumerated on (cc_options.stream, which must still exist),
+ * ordered after the enumeration.  Page-locked `vertices` buffers are filled by one DMA; pageable
+ * ones through two pinned staging buffers, the copy of one chunk overlapping the next chunk's DMA.
  */
 cc_status cc_fetch_cycles(const cc_result *r, uint64_t first, uint64_t max_cycles, int32_t *vertices,
                           size_t vertices_cap, uint64_t *offsets, uint64_t *n_fetched);

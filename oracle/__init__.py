@@ -127,7 +127,7 @@ def triplets(n, row_ptr, col, labels=None):
 
 def enumerate_cycles(n, row_ptr, col, max_len: int = 0, seed: int = DEFAULT_SEED, labels=None,
                      nthreads: int = 1, collect: bool = False, root_stride: int = 1,
-                     root_offset: int = 0, collect_cap: int = 1 << 20):
+                     root_offset: int = 0, collect_cap: int = 1 << 20, raw: bool = False):
     """Run Alg. 1.  Returns a dict with
 
     counts (uint64[n+1], counts[k] = #chordless cycles with k vertices), set_hash,
@@ -156,14 +156,17 @@ def enumerate_cycles(n, row_ptr, col, max_len: int = 0, seed: int = DEFAULT_SEED
     if rc == -6 and collect:
         return enumerate_cycles(n, row_ptr, col, max_len, seed, labels, nthreads, collect,
                                 root_stride, root_offset,
-                                collect_cap=max(2 * collect_cap, int(ncyc[0]) + 16))
+                                collect_cap=max(2 * collect_cap, int(ncyc[0]) + 16), raw=raw)
     if rc != 0:
         raise OracleError(rc)
     out = dict(counts=counts, set_hash=int(h[0]), paths_by_len=pbl, candidates=int(cand[0]),
                n_cycles=int(ncyc[0]))
     if collect:
         k = int(ncyc[0])
-        out["cycles"] = [verts[int(offs[i]):int(offs[i + 1])].tolist() for i in range(k)]
+        if raw:  # the same sequences as flat arrays (vertices, offsets[k + 1])
+            out["vertices"], out["offsets"] = verts[:int(offs[k])], offs[:k + 1]
+        else:
+            out["cycles"] = [verts[int(offs[i]):int(offs[i + 1])].tolist() for i in range(k)]
     return out
 
 

@@ -16,6 +16,8 @@
 #include "../../include/chordless.h"
 #include "cc_internal.h"
 
+#include <nvtx3/nvToolsExt.h>
+
 #include <algorithm>
 #include <functional>
 #include <chrono>
@@ -28,6 +30,7 @@
 #include <mutex>
 #include <set>
 #include <string>
+#include <thread>
 #include <vector>
 
 using cc::u64;
@@ -471,6 +474,7 @@ struct cc_result {
     cc_stats stats{};
     bool collected = false;
     int device = -1;
+    cudaStream_t stream = nullptr;  // cc_options.stream of the enumeration (cc_fetch_cycles uses it)
     int nw = 1;
     void *cyc_buf = nullptr;     // CycleStore s | ids, then adj copy, orig copy
     cc::CycleStore cyc{};
@@ -645,6 +649,7 @@ static cc_status enumerate_impl(const cc_graph *cg, const cc_options *opt_in, cc
     res->paths.assign(n + 2, 0);
     res->cand.assign(n + 2, 0);
     res->device = device;
+    res->stream = st;
     res->nw = std::max(g->nw, 1);
     res->collected = opt.collect != 0;
     cc_stats &S = res->stats;
@@ -878,6 +883,12 @@ static cc_status enumerate_impl(const cc_graph *cg, const cc_options *opt_in, cc
         a.filter = filter ? 1 : 0;
         if (opt.profile)
             CC_CUDA(cudaEventRecord(ea, st));
+        // NVTX range per launch ("expand L<t> f<fuse>", "stage1", "filter L<t>"): profilers can
+        // select one level, e.g. ncu --nvtx --nvtx-include "expand L44 f2/" (tools/)
+        char nv[48];
+        std::snprintf(nv, sizeof(nv), "%s L%d f%d", kind == STAGE1 ? "stage1" : kind == EXPAND ? "expand" : "filter",
+                      trace_level, fuse);
+        nvtxRangePushA(nv);
         a.tlen = (uint32_t)trace_level;  // vertices per input path of an expansion
         if (list)
             CC_CUDA(cc::launch_list(kind == STAGE1 ? 0 : kind == EXPAND ? 1 : 2, a, rwl, leaf, st,
@@ -899,6 +910,7 @@ static cc_status enumerate_impl(const cc_graph *cg, const cc_options *opt_in, cc
             CC_CUDA(cc::launch_shard_filter(a, mode, st, grid_sf));
         if (opt.profile)
             CC_CUDA(cudaEventRecord(eb, st));
+        nvtxRangePop();
         CC_CUDA(cudaMemcpyAsync(h_sc, d_sc, sizeof(cc::Scratch), cudaMemcpyDeviceToHost, st));
         CC_CUDA(cudaStreamSynchronize(st));
         S.d2h_bytes += sizeof(cc::Scratch);
@@ -991,9 +1003,20 @@ static cc_status enumerate_impl(const cc_graph *cg, const cc_options *opt_in, cc
         Level &L = levels[d];
         // ---- small frontiers: the first levels in one cooperative launch (no host round trip
         //      per level); the level where the frontier grows past a page is handed back here
+        // two regions of rk contiguous free pages each (the free list is in page order at this
+        // point); one page each when contiguity is not available
+        size_t rk = std::min<size_t>(16, free_pages.size() / 4);
+        if (small_ok && !small_tried && d == 3) {
+            const size_t fs = free_pages.size();
+            for (size_t i = 0; i < 2 * rk && rk > 1; ++i)
+                if (free_pages[fs - 1 - i] != free_pages[fs - 1] + i)
+                    rk = 1;
+        }
+        const u64 small_thr = (u64)std::max<size_t>(rk, 1) * P / (u64)std::max<int64_t>(1, g->max_deg - 1);
         if (small_ok && !small_tried && d == 3 && s1_next >= stage1_total && L.pages.size() == 1 &&
-            !free_pages.empty() && L.count <= P / (u64)std::max<int64_t>(1, g->max_deg - 1)) {
+            free_pages.size() >= 2 && L.count <= small_thr) {
             small_tried = true;
+            rk = std::max<size_t>(rk, 1);
             const size_t na = (size_t)n + 3;
             DevBuf sm;
             sm.st = st;
@@ -1002,15 +1025,21 @@ static cc_status enumerate_impl(const cc_graph *cg, const cc_options *opt_in, cc
             u64 *d_count = (u64 *)sm.p, *d_cyc = d_count + na, *d_cand = d_cyc + na, *d_misc = d_cand + na;
             const u64 c3 = L.count;
             CC_CUDA(cudaMemcpyAsync(d_count + 3, &c3, 8, cudaMemcpyHostToDevice, st));
-            const uint32_t pg0 = free_pages.back();
-            free_pages.pop_back();
+            std::vector<uint32_t> reg[2];
+            for (int r = 0; r < 2; ++r)
+                for (size_t i = 0; i < rk; ++i) {
+                    reg[r].push_back(free_pages.back());
+                    free_pages.pop_back();
+                }
             cc::SmallArgs sa{};
-            sa.page[0] = pg0;
-            sa.page[1] = L.pages[0];
+            sa.first = L.pages[0];
+            sa.region[0] = reg[0][0];
+            sa.region[1] = reg[1][0];
+            sa.region_cap = (u64)rk * P;
             sa.d0 = 3;
             sa.d_stop = max_len == 0 ? (int)n + 2 : (int)max_len - 2;  // leaf levels stay paged
             sa.max_len = max_len;
-            sa.threshold = P / (u64)std::max<int64_t>(1, g->max_deg - 1);  // children fit a page
+            sa.threshold = small_thr;  // the children of a level up to this size fit a region
             sa.count = d_count;
             sa.cyc = d_cyc;
             sa.cand = d_cand;
@@ -1052,21 +1081,34 @@ static cc_status enumerate_impl(const cc_graph *cg, const cc_options *opt_in, cc
                 S.paths_written += hc[t + 1];
                 S.rounds = std::max<u64>(S.rounds, (u64)t);
             }
-            // the level `last` (possibly empty) continues on the paged path
-            const uint32_t keep = last & 1 ? L.pages[0] : pg0, drop = last & 1 ? pg0 : L.pages[0];
-            free_pages.push_back(drop);
+            // the level `last` (possibly empty) continues on the paged path: it keeps the pages
+            // that hold it, every other page goes back to the free list
+            std::vector<uint32_t> keep;
+            const u64 nlast = hc[last];
+            if (last == 3) {
+                keep = L.pages;
+            } else {
+                free_pages.push_back(L.pages[0]);
+                keep = reg[(last - 4) & 1];
+                keep.resize((size_t)((nlast + P - 1) / P));
+            }
+            for (int r = 0; r < 2; ++r)
+                for (uint32_t pgi : reg[r])
+                    if (std::find(keep.begin(), keep.end(), pgi) == keep.end())
+                        free_pages.push_back(pgi);
             in_use -= L.count;
             L.pages.clear();
             L.count = 0;
             Level &N = levels[last];
-            N.pages.assign(1, keep);
-            N.count = hc[last];
+            N.pages = keep;
+            N.count = nlast;
             N.sharded = true;  // W == 1 only
             N.shard_now = false;
             in_use += N.count;
             high_water = std::max(high_water, in_use);
             if (N.count == 0) {
-                free_pages.push_back(keep);
+                for (uint32_t pgi : N.pages)
+                    free_pages.push_back(pgi);
                 N.pages.clear();
             }
             deepest = last;
@@ -1348,6 +1390,64 @@ extern "C" cc_status cc_result_stats(const cc_result *r, cc_stats *out)
     return CC_OK;
 }
 
+// Host side of a device->host copy into the caller's buffer: when `dst` is pageable, the bytes
+// stream through two pinned staging buffers -- the DMA of chunk i+1 overlaps the host copy
+// (several threads) of chunk i out of the other buffer; pinned (page-locked or registered)
+// destinations are copied directly.
+static cudaError_t d2h_stream(void *dst, const void *src, size_t bytes, cudaStream_t st)
+{
+    if (bytes == 0)
+        return cudaSuccess;
+    cudaPointerAttributes at{};
+    if (cudaPointerGetAttributes(&at, dst) == cudaSuccess && at.type == cudaMemoryTypeHost) {
+        cudaError_t e = cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDeviceToHost, st);
+        return e == cudaSuccess ? cudaStreamSynchronize(st) : e;
+    }
+    cudaGetLastError();  // pageable memory: cudaPointerGetAttributes may report an error
+    constexpr size_t kChunk = 64ull << 20;
+    static thread_local Pinned stage;
+    cudaError_t e = stage.reserve(2 * kChunk);
+    if (e != cudaSuccess)
+        return e;
+    cudaEvent_t done[2];
+    cudaEventCreateWithFlags(&done[0], cudaEventDisableTiming);
+    cudaEventCreateWithFlags(&done[1], cudaEventDisableTiming);
+    const size_t nch = (bytes + kChunk - 1) / kChunk;
+    auto issue = [&](size_t i) {
+        const size_t off = i * kChunk, len = std::min(kChunk, bytes - off);
+        char *buf = (char *)stage.p + (i & 1) * kChunk;
+        cudaError_t r = cudaMemcpyAsync(buf, (const char *)src + off, len, cudaMemcpyDeviceToHost, st);
+        if (r == cudaSuccess)
+            r = cudaEventRecord(done[i & 1], st);
+        return r;
+    };
+    e = issue(0);
+    for (size_t i = 0; i < nch && e == cudaSuccess; ++i) {
+        if (i + 1 < nch)
+            e = issue(i + 1);  // the other buffer was drained by the host copy of chunk i-1
+        if (e == cudaSuccess)
+            e = cudaEventSynchronize(done[i & 1]);
+        if (e != cudaSuccess)
+            break;
+        const size_t off = i * kChunk, len = std::min(kChunk, bytes - off);
+        const char *buf = (const char *)stage.p + (i & 1) * kChunk;
+        // host copy out of the pinned buffer on 4 threads
+        constexpr int kT = 4;
+        std::vector<std::thread> th;
+        const size_t per = (len + kT - 1) / kT;
+        for (int t = 0; t < kT; ++t) {
+            const size_t lo = std::min(len, t * per), hi = std::min(len, lo + per);
+            if (hi > lo)
+                th.emplace_back([=] { std::memcpy((char *)dst + off + lo, buf + lo, hi - lo); });
+        }
+        for (auto &x : th)
+            x.join();
+    }
+    cudaEventDestroy(done[0]);
+    cudaEventDestroy(done[1]);
+    return e;
+}
+
 extern "C" cc_status cc_fetch_cycles(const cc_result *r, uint64_t first, uint64_t max_cycles, int32_t *vertices,
                                      size_t vertices_cap, uint64_t *offsets, uint64_t *n_fetched)
 {
@@ -1372,14 +1472,17 @@ extern "C" cc_status cc_fetch_cycles(const cc_result *r, uint64_t first, uint64_
                 cudaSetDevice(d);
         }
     } restore{cur};
-    cudaStream_t st = nullptr;
-    // scratch from the stream-ordered pool (reused across batches, no device-wide sync)
+    // the stream the result was enumerated on (cc_options.stream), so the fetch is ordered after
+    // the enumeration without a device-wide synchronisation
+    cudaStream_t st = r->stream;
+    // scratch from the library's stream-ordered pool (reused across batches)
     uint32_t *d_len = nullptr;
     CC_CUDA(pool_alloc((void **)&d_len, cnt * 4, r->device, st));
-    std::vector<uint32_t> len(cnt);
+    CC_CUDA(t_pinned.reserve(cnt * 4 + 64));
+    uint32_t *len = (uint32_t *)t_pinned.p;
     cudaError_t e = cc::launch_cycle_lengths(r->cyc, r->nw, first, cnt, d_len, st);
     if (e == cudaSuccess)
-        e = cudaMemcpyAsync(len.data(), d_len, cnt * 4, cudaMemcpyDeviceToHost, st);
+        e = cudaMemcpyAsync(len, d_len, cnt * 4, cudaMemcpyDeviceToHost, st);
     cudaFreeAsync(d_len, st);
     if (e == cudaSuccess)
         e = cudaStreamSynchronize(st);
@@ -1400,7 +1503,7 @@ extern "C" cc_status cc_fetch_cycles(const cc_result *r, uint64_t first, uint64_
     if (e == cudaSuccess)
         e = cc::launch_cycle_sequences(r->cyc, r->nw, r->adj, r->orig, first, cnt, d_off, d_v, st);
     if (e == cudaSuccess)
-        e = cudaMemcpyAsync(vertices, d_v, total * 4, cudaMemcpyDeviceToHost, st);
+        e = d2h_stream(vertices, d_v, total * 4, st);
     cudaFreeAsync(d_off, st);
     cudaFreeAsync(d_v, st);
     if (e == cudaSuccess)

@@ -148,16 +148,20 @@ cudaError_t launch_keys(u64 *key, u64 *keybyte, const int32_t *orig, int n, int 
 // between levels, ping-ponging between two arena pages; it stops (hands the current level to
 // the paged scheduler) when a level could outgrow a page or reaches the last (leaf) level.
 struct SmallArgs {
-    uint32_t page[2];            // the two arena pages (level d lives in page[d & 1])
-    int32_t d0;                  // first level (3: the triplets, in page[1])
+    uint32_t first;              // the arena page holding level d0 (the triplets)
+    uint32_t region[2];          // first pages of two runs of `region_pages` contiguous pages:
+                                 // level d > d0 lives in region[(d - d0 - 1) & 1]
+    uint64_t region_cap;         // records per region (region_pages * P)
+    int32_t d0;                  // first level (3: the triplets)
     int32_t d_stop;              // levels d0 .. d_stop-1 may run here (leaf levels excluded)
     uint32_t max_len;            // cc_options.max_len
-    u64 threshold;               // a level with more input paths is handed off
+    u64 threshold;               // a level with more input paths is handed off (its children
+                                 // might not fit a region)
     u64 *count;                  // [n+3] count[d] = |F_d| written (count[d0] set by the host)
     u64 *cyc;                    // [n+3] closures of length d+1 found at level d
     u64 *cand;                   // [n+3] candidate slots of level d
     u64 *hash;                   // sum of h(C)
-    int32_t *last;               // the level the kernel stopped at (its records are in page[last & 1])
+    int32_t *last;               // the level the kernel stopped at
     u64 *err;                    // overflow (must stay 0: the threshold guarantees room)
 };
 cudaError_t launch_small(const LaunchArgs &a, const SmallArgs &s, cudaStream_t st, int sms);

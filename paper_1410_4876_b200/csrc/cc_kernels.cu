@@ -761,8 +761,10 @@ __global__ void __launch_bounds__(kBlock) k_small_levels(const LaunchArgs p, con
         const u64 n_in = s.count[d];
         if (n_in == 0 || d >= s.d_stop || n_in > s.threshold)
             break;  // block-uniform: everybody read the same count after the barrier
-        const char *ip = p.pg.base + (u64)s.page[d & 1] * p.pg.page_bytes;
-        char *op = p.pg.base + (u64)s.page[(d + 1) & 1] * p.pg.page_bytes;
+        // level d: the triplets' page or a region of contiguous pages (record r in page
+        // region + (r >> log_p), slot r & (P - 1)); its children go to the other region
+        const uint32_t ipg = d == s.d0 ? s.first : s.region[(d - s.d0 - 1) & 1];
+        const uint32_t opg = s.region[(d - s.d0) & 1];
         const bool emit = s.max_len == 0 || (u64)d + 1 < s.max_len;
         uint32_t cnt = 0, cand = 0;
         u64 hs = 0;
@@ -775,10 +777,12 @@ __global__ void __launch_bounds__(kBlock) k_small_levels(const LaunchArgs p, con
             for (int w = 0; w < NW; ++w)
                 ext[w] = 0;
             if (r < n_in) {
+                const char *ip = p.pg.base + (u64)(ipg + (uint32_t)(r >> p.pg.log_p)) * p.pg.page_bytes;
+                const u64 rs_ = r & (P - 1);
 #pragma unroll
                 for (int w = 0; w < RW; ++w)
-                    W[w] = ((const u64 *)ip)[(u64)w * P + r];
-                id = PACK ? (uint32_t)packed_ids(W[NW - 1], idb) : ((const uint32_t *)(ip + (u64)RW * P * 8))[r];
+                    W[w] = ((const u64 *)ip)[(u64)w * P + rs_];
+                id = PACK ? (uint32_t)packed_ids(W[NW - 1], idb) : ((const uint32_t *)(ip + (u64)RW * P * 8))[rs_];
                 const uint32_t v1 = id & idm, v2 = (id >> idb) & idm, vt = id >> (2 * idb);
                 u64 arow[NW], abv[NW], a1[NW];
                 lds_row<NW>(s_adj, vt, arow);
@@ -802,7 +806,7 @@ __global__ void __launch_bounds__(kBlock) k_small_levels(const LaunchArgs p, con
             }
             const u64 off = block_reserve(ne, &s.count[d + 1], rs);
             if (ne) {
-                if (off + ne > P) {
+                if (off + ne > s.region_cap) {
                     *s.err = 1;
                 } else {
                     const uint32_t vt = id >> (2 * idb), v12 = id & ((1u << (2 * idb)) - 1);
@@ -824,13 +828,15 @@ __global__ void __launch_bounds__(kBlock) k_small_levels(const LaunchArgs p, con
                             for (int q = 0; q < RW; ++q)
                                 X[q] = C[q];
                             X[NW] = W[NW] + s_key[v];
+                            char *op = p.pg.base + (u64)(opg + (uint32_t)(o >> p.pg.log_p)) * p.pg.page_bytes;
+                            const u64 os_ = o & (P - 1);
                             if (PACK)
                                 X[NW - 1] |= (u64)v << (64 - idb);
                             else
-                                ((uint32_t *)(op + (u64)RW * P * 8))[o] = v12 | (v << (2 * idb));
+                                ((uint32_t *)(op + (u64)RW * P * 8))[os_] = v12 | (v << (2 * idb));
 #pragma unroll
                             for (int q = 0; q < RW; ++q)
-                                ((u64 *)op)[(u64)q * P + o] = X[q];
+                                ((u64 *)op)[(u64)q * P + os_] = X[q];
                             ++o;
                         }
                     }

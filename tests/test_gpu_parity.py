@@ -409,6 +409,9 @@ def test_k150_collect_at_scale(ws):
     codes = np.concatenate(codes)
     assert len(np.unique(codes)) == total
     assert hs == h
+    # ... and equals the oracle's set hash of the whole graph (tests/golden/oracle_k150.json)
+    import json
+    assert f"{h:#018x}" == json.load(open(os.path.join(GOLDEN, "oracle_k150.json")))["set_hash"]
 
 
 GOLDEN = os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden")
@@ -557,3 +560,37 @@ def test_fused_kernel_small_arena_chunks(ws, kb):
     assert sum(p["counts"] for p in parts).tolist() == want["counts"].tolist()
     assert sum(p["set_hash"] for p in parts) % (1 << 64) == want["set_hash"]
     assert sum(p["paths_by_len"] for p in parts).tolist() == want["paths_by_len"].tolist()
+
+
+def _cycle_codes(verts, offs, n):
+    """Per cycle: the vertex set as an n-bit mask (n <= 64) and a position-weighted hash of the
+    canonical sequence -- to compare two cycle lists of 10^6 entries with numpy."""
+    verts = np.asarray(verts, dtype=np.uint64)
+    offs = np.asarray(offs, dtype=np.int64)
+    k = len(offs) - 1
+    cyc = np.repeat(np.arange(k), np.diff(offs))
+    pos = np.arange(len(verts), dtype=np.int64) - offs[:-1][cyc]
+    mask = np.bitwise_or.reduceat(np.left_shift(np.uint64(1), verts), offs[:-1])
+    w = (verts + np.uint64(1)) * ((pos.astype(np.uint64) * np.uint64(0x9E3779B97F4A7C15)) | np.uint64(1))
+    seq = np.add.reduceat(w, offs[:-1])
+    return mask, seq
+
+
+def test_p8x8_collect_list_equals_oracle(ws):
+    """P8xP8 in collect mode (1,743,247 cycles): the fetched cycle list equals the
+    oracle's, as vertex sets and as canonical sequences (same labelling on both sides)."""
+    import json
+    g = I.grid(8, 8)
+    gr = binding.cc_graph_from_csr(*g)
+    r = binding.cc_enumerate(gr, collect=True, workspace=ws)
+    counts, h = binding.cc_count_by_length(r)
+    want = oracle.enumerate_cycles(*g, collect=True, raw=True, collect_cap=1 << 21)
+    assert counts.tolist() == want["counts"].tolist() and h == want["set_hash"]
+    assert f"{h:#018x}" == json.load(open(os.path.join(GOLDEN, "oracle_p8x8.json")))["set_hash"]
+    verts, offs = binding.cc_fetch_cycles(r)
+    gm, gs = _cycle_codes(verts, offs, 64)
+    wm, wsq = _cycle_codes(want["vertices"], want["offsets"], 64)
+    assert len(gm) == len(wm) == 1743247
+    assert len(np.unique(gm)) == len(gm)  # exactly once
+    assert np.array_equal(np.sort(gm), np.sort(wm))
+    assert np.array_equal(np.sort(gs), np.sort(wsq))
