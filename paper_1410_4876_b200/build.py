@@ -27,7 +27,22 @@ def stale() -> bool:
     return any(os.path.getmtime(f) > t for f in SOURCES + HEADERS)
 
 
-def build(force: bool = False, verbose: bool = False) -> str:
+def build(force: bool = False, verbose: bool = False, out: str | None = None, extra=()) -> str:
+    """Compile every translation unit and link `out` (default: the in-tree libchordless.so).
+    `extra` nvcc flags build A/B variants (e.g. ["-DCC_FUSED_MINB=3"], out=...variant.so)."""
+    global EXTRA
+    lib = out or LIB
+    if out or extra:
+        force = True
+    saved = EXTRA
+    EXTRA = EXTRA + list(extra)
+    try:
+        return _build(force, verbose, lib)
+    finally:
+        EXTRA = saved
+
+
+def _build(force: bool, verbose: bool, LIB: str) -> str:
     if force or stale():
         tag = f".tmp{os.getpid()}"
         objs, procs = [], []
@@ -56,4 +71,11 @@ def build(force: bool = False, verbose: bool = False) -> str:
 
 
 if __name__ == "__main__":
-    print(build(force="--force" in sys.argv, verbose=True))
+    # python -m paper_1410_4876_b200.build [--force] [--out path.so] [nvcc flags ...]
+    args = sys.argv[1:]
+    force = "--force" in args
+    out = None
+    if "--out" in args:
+        out = args[args.index("--out") + 1]
+    extra = [a for a in args if a.startswith("-D")]
+    print(build(force=force, verbose=True, out=out, extra=extra))

@@ -124,8 +124,11 @@ __device__ __forceinline__ void put_record(char *pp, uint32_t slot, uint32_t log
         ((uint32_t *)(pp + ((u64)RW << log_p) * 8))[slot] = id;
 }
 
+#ifndef CC_FUSED_MINB
+#define CC_FUSED_MINB 4  // resident CTAs per SM the register allocation must allow (4: 64 registers)
+#endif
 template <int NW, bool PACK, int FUSE, bool LEAF>
-__global__ void __launch_bounds__(kFBlock, 4) k_expand_fused(const LaunchArgs p, const uint32_t log_ch)
+__global__ void __launch_bounds__(kFBlock, CC_FUSED_MINB) k_expand_fused(const LaunchArgs p, const uint32_t log_ch)
 {
     static_assert(FUSE == 1 || !LEAF, "last-level fusion is single-level");
     constexpr int RW = NW + 1;

@@ -66,6 +66,12 @@ double now_ms()
 
 }  // namespace
 
+// the library's private stream-ordered pool (defined below)
+namespace {
+cudaError_t pool_alloc(void **p, size_t bytes, int device, cudaStream_t st);
+cudaMemPool_t lib_pool(int device);
+}
+
 // ------------------------------------------------------------------------------ graph
 struct DevCopy {
     int device = -1;
@@ -348,7 +354,7 @@ extern "C" void cc_graph_free(cc_graph *g)
     for (auto &d : g->dev)
         if (d.buf) {
             cudaSetDevice(d.device);
-            cudaFree(d.buf);
+            cudaFreeAsync(d.buf, 0);  // stream-ordered: no device-wide synchronisation
         }
     if (cur >= 0)
         cudaSetDevice(cur);
@@ -396,7 +402,7 @@ static cc_status ensure_device_graph(cc_graph *g, int device, u64 seed, cudaStre
         cc_status s = upload_graph(g, device, st, &nd, h2d);
         if (s != CC_OK) {
             if (nd.buf)
-                cudaFree(nd.buf);
+                cudaFreeAsync(nd.buf, st);
             return s;
         }
         g->dev.push_back(nd);
@@ -425,7 +431,9 @@ static cc_status upload_graph(cc_graph *g, int device, cudaStream_t st, DevCopy 
         const bool want_nm = g->wide && g->max_deg <= 32;
         const size_t s_nm = want_nm ? align_up((size_t)n * n * 4, 256) : 0;
         dc->bytes = s_row + s_col + s_fwd + s_pp + s_adj + s_orig + s_key + s_kb + s_nm;
-        CC_CUDA(cudaMalloc(&dc->buf, dc->bytes));
+        // from the library's pool: a fresh graph per call (the e2e path) then reuses the same
+        // memory without cudaMalloc / cudaFree, each of which synchronises the whole device
+        CC_CUDA(pool_alloc(&dc->buf, dc->bytes, device, st));
         char *p = (char *)dc->buf;
         auto *rowptr = (uint32_t *)p; p += s_row;
         auto *col = (uint32_t *)p; p += s_col;
@@ -491,7 +499,10 @@ extern "C" void cc_result_free(cc_result *r)
         int cur = -1;
         cudaGetDevice(&cur);
         cudaSetDevice(r->device);
-        cudaFree(r->cyc_buf);
+        cudaFreeAsync(r->cyc_buf, r->stream);
+        // collect stores can be gigabytes: return them to the driver, not to the pool's cache
+        cudaStreamSynchronize(r->stream);
+        cudaMemPoolTrimTo(lib_pool(r->device), 256ull << 20);
         if (cur >= 0)
             cudaSetDevice(cur);
     }
@@ -740,7 +751,7 @@ static cc_status enumerate_impl(const cc_graph *cg, const cc_options *opt_in, cc
         const u64 ccap = opt.collect_capacity ? opt.collect_capacity : (1ull << 22);
         const size_t s_s = align_up(ccap * nw * 8, 256), s_ids = align_up(ccap * 4, 256),
                      s_adj = align_up((size_t)n * nw * 8, 256), s_orig = align_up((size_t)n * 4, 256);
-        CC_CUDA(cudaMalloc(&res->cyc_buf, s_s + s_ids + s_adj + s_orig));
+        CC_CUDA(pool_alloc(&res->cyc_buf, s_s + s_ids + s_adj + s_orig, device, st));
         char *p = (char *)res->cyc_buf;
         res->cyc.s = (u64 *)p;
         res->cyc.ids = (uint32_t *)(p + s_s);
@@ -1475,41 +1486,38 @@ extern "C" cc_status cc_fetch_cycles(const cc_result *r, uint64_t first, uint64_
     // the stream the result was enumerated on (cc_options.stream), so the fetch is ordered after
     // the enumeration without a device-wide synchronisation
     cudaStream_t st = r->stream;
-    // scratch from the library's stream-ordered pool (reused across batches)
-    uint32_t *d_len = nullptr;
-    CC_CUDA(pool_alloc((void **)&d_len, cnt * 4, r->device, st));
-    CC_CUDA(t_pinned.reserve(cnt * 4 + 64));
-    uint32_t *len = (uint32_t *)t_pinned.p;
-    cudaError_t e = cc::launch_cycle_lengths(r->cyc, r->nw, first, cnt, d_len, st);
-    if (e == cudaSuccess)
-        e = cudaMemcpyAsync(len, d_len, cnt * 4, cudaMemcpyDeviceToHost, st);
-    cudaFreeAsync(d_len, st);
-    if (e == cudaSuccess)
-        e = cudaStreamSynchronize(st);
-    if (e != cudaSuccess)
-        return cuda_fail(e, "cycle lengths");
-    offsets[0] = 0;
-    for (u64 i = 0; i < cnt; ++i)
-        offsets[i + 1] = offsets[i] + len[i];
-    const u64 total = offsets[cnt];
-    if (total > vertices_cap || !vertices)
-        return fail(CC_ERR_BUFFER_TOO_SMALL, "vertices needs " + std::to_string(total) + " entries");
-    u64 *d_off = nullptr;
+    // offsets (a device scan of the cycle lengths), then the canonical sequences, both copied
+    // back through d2h_stream; scratch from the library's stream-ordered pool
+    const u64 nblk = (cnt + 1023) / 1024;
+    u64 *d_off = nullptr, *d_blk = nullptr;
     int32_t *d_v = nullptr;
     CC_CUDA(pool_alloc((void **)&d_off, (cnt + 1) * 8, r->device, st));
-    e = pool_alloc((void **)&d_v, std::max<u64>(total, 1) * 4, r->device, st);
+    cudaError_t e = pool_alloc((void **)&d_blk, (nblk + 1) * 8, r->device, st);
     if (e == cudaSuccess)
-        e = cudaMemcpyAsync(d_off, offsets, (cnt + 1) * 8, cudaMemcpyHostToDevice, st);
+        e = cc::launch_cycle_offsets(r->cyc, r->nw, first, cnt, d_off, d_blk, st);
+    u64 total = 0;
     if (e == cudaSuccess)
+        e = cudaMemcpyAsync(&total, d_off + cnt, 8, cudaMemcpyDeviceToHost, st);
+    if (e == cudaSuccess)
+        e = cudaStreamSynchronize(st);
+    if (e == cudaSuccess && total <= vertices_cap && vertices)
+        e = pool_alloc((void **)&d_v, std::max<u64>(total, 1) * 4, r->device, st);
+    if (e == cudaSuccess && d_v)
         e = cc::launch_cycle_sequences(r->cyc, r->nw, r->adj, r->orig, first, cnt, d_off, d_v, st);
     if (e == cudaSuccess)
+        e = d2h_stream(offsets, d_off, (cnt + 1) * 8, st);
+    if (e == cudaSuccess && d_v)
         e = d2h_stream(vertices, d_v, total * 4, st);
     cudaFreeAsync(d_off, st);
-    cudaFreeAsync(d_v, st);
+    cudaFreeAsync(d_blk, st);
+    if (d_v)
+        cudaFreeAsync(d_v, st);
     if (e == cudaSuccess)
         e = cudaStreamSynchronize(st);
     if (e != cudaSuccess)
         return cuda_fail(e, "cycle sequences");
+    if (total > vertices_cap || !vertices)
+        return fail(CC_ERR_BUFFER_TOO_SMALL, "vertices needs " + std::to_string(total) + " entries");
     *n_fetched = cnt;
     return CC_OK;
 }

@@ -169,6 +169,10 @@ cudaError_t launch_small(const LaunchArgs &a, const SmallArgs &s, cudaStream_t s
 cudaError_t launch_nbrmask(const DevGraph &g, uint32_t *T, cudaStream_t st);
 cudaError_t launch_cycle_lengths(const CycleStore &c, int nw, uint64_t first, uint64_t count,
                                  uint32_t *len, cudaStream_t st);
+// off[0..count] = exclusive prefix sums of the lengths of stored cycles first..first+count-1
+// (off[count] = total); blk = scratch of ceil(count / 1024) + 1 words
+cudaError_t launch_cycle_offsets(const CycleStore &c, int nw, uint64_t first, uint64_t count, u64 *off, u64 *blk,
+                                 cudaStream_t st);
 cudaError_t launch_cycle_sequences(const CycleStore &c, int nw, const u64 *adj, const int32_t *orig,
                                    uint64_t first, uint64_t count, const u64 *offsets,
                                    int32_t *out, cudaStream_t st);

@@ -1770,6 +1770,115 @@ __global__ void k_cycle_lengths(const CycleStore c, int nw, uint64_t first, uint
     len[i] = k;
 }
 
+// Offsets of the fetched cycles on the device: off[i] = sum of the lengths of cycles first ..
+// first+i-1 (off[count] = total).  Three passes: per-1024-block exclusive scans with block sums,
+// one block scanning the block sums, then the block prefixes added.
+constexpr int kScanBlock = 1024;
+
+__global__ void __launch_bounds__(kScanBlock) k_cycle_scan_blocks(const CycleStore c, int nw, uint64_t first,
+                                                                  uint64_t count, u64 *off, u64 *blk)
+{
+    __shared__ u64 ws[kScanBlock / 32];
+    const u64 i = (u64)blockIdx.x * kScanBlock + threadIdx.x;
+    u64 k = 0;
+    if (i < count)
+        for (int w = 0; w < nw; ++w)
+            k += __popcll(c.s[(u64)w * c.cap + first + i]);
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    u64 incl = k;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const u64 v = __shfl_up_sync(FULL_MASK, incl, o);
+        if (lane >= o)
+            incl += v;
+    }
+    if (lane == 31)
+        ws[wid] = incl;
+    __syncthreads();
+    if (wid == 0) {
+        u64 x = ws[lane];
+        u64 xi = x;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const u64 v = __shfl_up_sync(FULL_MASK, xi, o);
+            if (lane >= o)
+                xi += v;
+        }
+        ws[lane] = xi - x;
+        if (lane == 31)
+            blk[blockIdx.x] = xi;
+    }
+    __syncthreads();
+    if (i < count)
+        off[i] = ws[wid] + incl - k;
+}
+
+__global__ void __launch_bounds__(kScanBlock) k_cycle_scan_tops(u64 *blk, uint64_t nblk, u64 *total)
+{
+    // one block: exclusive scan of nblk block sums, kScanBlock at a time
+    __shared__ u64 ws[kScanBlock / 32];
+    __shared__ u64 carry;
+    if (threadIdx.x == 0)
+        carry = 0;
+    __syncthreads();
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    for (u64 b = 0; b < nblk; b += kScanBlock) {
+        const u64 i = b + threadIdx.x;
+        const u64 k = i < nblk ? blk[i] : 0;
+        u64 incl = k;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const u64 v = __shfl_up_sync(FULL_MASK, incl, o);
+            if (lane >= o)
+                incl += v;
+        }
+        if (lane == 31)
+            ws[wid] = incl;
+        __syncthreads();
+        if (wid == 0) {
+            u64 x = ws[lane], xi = x;
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                const u64 v = __shfl_up_sync(FULL_MASK, xi, o);
+                if (lane >= o)
+                    xi += v;
+            }
+            ws[lane] = xi - x;
+        }
+        __syncthreads();
+        const u64 c0 = carry;
+        if (i < nblk)
+            blk[i] = c0 + ws[wid] + incl - k;
+        __syncthreads();
+        if (threadIdx.x == kScanBlock - 1)
+            carry = c0 + ws[wid] + incl;
+        __syncthreads();
+    }
+    if (threadIdx.x == 0)
+        *total = carry;
+}
+
+__global__ void k_cycle_scan_add(u64 *off, const u64 *blk, uint64_t count, const u64 *total)
+{
+    const u64 i = (u64)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < count)
+        off[i] += blk[i / kScanBlock];
+    else if (i == count)
+        off[count] = *total;
+}
+
+cudaError_t launch_cycle_offsets(const CycleStore &c, int nw, uint64_t first, uint64_t count, u64 *off, u64 *blk,
+                                 cudaStream_t st)
+{
+    if (count == 0)
+        return cudaSuccess;
+    const u64 nblk = (count + kScanBlock - 1) / kScanBlock;
+    k_cycle_scan_blocks<<<(unsigned int)nblk, kScanBlock, 0, st>>>(c, nw, first, count, off, blk);
+    k_cycle_scan_tops<<<1, kScanBlock, 0, st>>>(blk, nblk, blk + nblk);
+    k_cycle_scan_add<<<(unsigned int)((count + 256) / 256), 256, 0, st>>>(off, blk, count, blk + nblk);
+    return cudaGetLastError();
+}
+
 // Walk the induced cycle S from v1 -> v2 -> ...: each vertex of a chordless cycle has exactly
 // two neighbours in S, so the successor of cur is the neighbour in S other than prev.
 __global__ void k_cycle_sequences(const CycleStore c, int nw, const u64 *adj, const int32_t *orig,
