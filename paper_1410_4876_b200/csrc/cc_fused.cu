@@ -430,6 +430,259 @@ __global__ void __launch_bounds__(kFBlock, CC_FUSED_MINB) k_expand_fused(const L
     flush<kFBlock>(a, p.sc);
 }
 
+// ---------------------------------------------------------------------------------------------
+// k_expand_fq: the same two-level expansion (F_t -> F_{t+2}, packed records) organised as full
+// 32-lane rounds.  A round is either an input round (32 paths of F_t, straight from the input
+// tiles) or a child round (32 paths of F_{t+1} popped from the warp's child queue).  Children of
+// an input round are pushed on the queue, children of a child round (F_{t+2}) on the warp's
+// output queue, which is written to HBM 32 records at a time (coalesced, per-warp chunks as in
+// k_expand_fused).  Child rounds run whenever the queue holds >= 32 paths, so every round but
+// the warp's last few uses all 32 lanes, and the queues stay below 32 + 96 records.  Records
+// in the queues are complete (B | N[vt] with v1, v2, vt packed, keysum): no parent references.
+constexpr int kQCap = 32 + kFCh1;   // child queue / output queue capacity (records)
+
+#ifndef CC_FQ_STAGES
+#define CC_FQ_STAGES 2
+#endif
+constexpr int kFqStages = CC_FQ_STAGES;  // input tiles in flight per warp (cp.async ring)
+
+template <int NW>
+struct FqWarpSmem {
+    static constexpr int RW = NW + 1;
+    u64 q[RW][kQCap];     // child queue (F_{t+1}), SoA
+    u64 o[RW][kQCap];     // output queue (F_{t+2}), SoA
+    u64 in[kFqStages][RW][32];  // input tiles, filled by cp.async (each lane copies its own record)
+};
+
+__device__ __forceinline__ void cp_async8(void *dst, const void *src)
+{
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(smem_u32(dst)), "l"(src) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
+
+template <int NW>
+__host__ __device__ constexpr size_t fq_warp_bytes()
+{
+    return (sizeof(FqWarpSmem<NW>) + 15) & ~(size_t)15;
+}
+
+template <int NW>
+__global__ void __launch_bounds__(kFBlock, CC_FUSED_MINB) k_expand_fq(const LaunchArgs p, const uint32_t log_ch)
+{
+    constexpr int RW = NW + 1;
+    using WS = FqWarpSmem<NW>;
+    constexpr uint32_t IDB = 5 + NW;  // packed records only (cc_host.cpp)
+    constexpr uint32_t IDM = (1u << IDB) - 1;
+    constexpr u64 KEEP_V12 = ~((u64)IDM << (64 - IDB));
+    extern __shared__ __align__(16) u64 smem[];
+    const int n = p.g.n;
+    u64 *s_adj = smem;                          // closed rows N[v] = Adj(v) | {v}
+    u64 *s_above = s_adj + n * NW;              // label gate {x : x > v}
+    u64 *s_key = s_above + n * NW;              // key(v)
+    char *wbase = (char *)(s_key + ((n + 1) & ~1));
+    WS &ws = *(WS *)(wbase + (threadIdx.x >> 5) * fq_warp_bytes<NW>());
+    for (int i = threadIdx.x; i < n * NW; i += kFBlock) {
+        s_above[i] = above_word((uint32_t)(i / NW), i % NW);
+        s_adj[i] = p.g.adj[i] | bit_in_word(i % NW, (uint32_t)(i / NW));
+    }
+    for (int i = threadIdx.x; i < n; i += kFBlock)
+        s_key[i] = p.g.key[i];
+    __syncthreads();
+
+    const int lane = threadIdx.x & 31;
+    const uint32_t log_p = p.pg.log_p;
+    const u64 nt = (p.n_in + 31) >> 5;
+    const u64 tw = (u64)gridDim.x * kFWarps;
+    WarpOut out;
+    uint32_t n_in = 0, cnt1 = 0, cand1 = 0, n_next = 0, cnt2 = 0, cand2 = 0, written = 0;
+    u64 hs = 0;
+    uint32_t nq = 0, no = 0;  // warp-uniform queue fills
+
+    // input tile k of this warp (global tile wt0 + k * tw) -> ring stage k % kFqStages; one
+    // commit group per tile, empty groups past the end keep the wait counts uniform
+    const u64 wt0 = blockIdx.x * (u64)kFWarps + (threadIdx.x >> 5);
+    auto issue = [&](u64 k) {
+        const u64 wt = wt0 + k * tw;
+        if (wt < nt) {
+            const u64 r0 = wt << 5;
+            const char *pp = page_ptr(p.pg, p.pg.in_pages[r0 >> log_p]);
+            const uint32_t slot = (uint32_t)(r0 & ((1ull << log_p) - 1)) + lane;
+            const int stg = (int)(k % kFqStages);
+#pragma unroll
+            for (int w = 0; w < RW; ++w)
+                cp_async8(&ws.in[stg][w][lane], (const u64 *)pp + ((u64)w << log_p) + slot);
+        }
+        cp_async_commit();
+    };
+    // write the 32 (or, at the end, fewer) records at the end of the output queue
+    auto flush_out = [&](uint32_t T) {
+        if (T == 0 || out.dead)
+            return;
+        char *pp0, *pp1;
+        uint32_t s0, s1, split;
+        warp_reserve(out, T, log_ch, p, pp0, s0, pp1, s1, split);
+        if (out.dead)
+            return;
+        written += T;
+        const uint32_t base = no - T;
+        for (uint32_t k = lane; k < T; k += 32) {
+            u64 C[RW];
+#pragma unroll
+            for (int w = 0; w < RW; ++w)
+                C[w] = ws.o[w][base + k];
+            const bool lo = k < split;
+            put_record<RW, true>(lo ? pp0 : pp1, lo ? s0 + k : s1 + (k - split), log_p, C, 0u);
+        }
+        no = base;
+    };
+
+    u64 W[RW];
+    u64 kin = 0;  // next input tile of this warp
+    bool have_in = wt0 < nt;
+#pragma unroll
+    for (int k = 0; k < kFqStages - 1; ++k)
+        issue((u64)k);
+    for (;;) {
+        // ---- pick the round: children first once 32 are queued (keeps the queue bounded)
+        bool child_round, valid;
+        if (nq >= 32 || (!have_in && nq > 0)) {
+            child_round = true;
+            const uint32_t take = nq < 32 ? nq : 32;
+            valid = (uint32_t)lane < take;
+            const uint32_t idx = nq - take + lane;
+            if (valid) {
+#pragma unroll
+                for (int w = 0; w < RW; ++w)
+                    W[w] = ws.q[w][idx];
+            }
+            nq -= take;
+        } else if (have_in) {
+            child_round = false;
+            cp_async_wait<kFqStages - 2>();  // tile kin has landed (this lane's own copies)
+            const int stg = (int)(kin % kFqStages);
+#pragma unroll
+            for (int w = 0; w < RW; ++w)
+                W[w] = ws.in[stg][w][lane];
+            const u64 r = ((wt0 + kin * tw) << 5) + lane;
+            issue(kin + kFqStages - 1);  // refill the stage read a round ago
+            ++kin;
+            have_in = wt0 + kin * tw < nt;
+            const uint32_t ids = (uint32_t)(W[NW - 1] >> (64 - 3 * IDB));
+            valid = r < p.n_in && (ids & IDM) != ((ids >> IDB) & IDM);  // empty slot: v1 == v2
+        } else {
+            break;
+        }
+        __syncwarp();  // queue slots just read may be overwritten by this round's pushes
+        // ---- expand the round's paths: test of Alg. 3 l.11-15 on the blocked set
+        u64 ext[NW], base_rec[NW];
+        uint32_t nc = 0;
+        u64 ks = W[NW];
+#pragma unroll
+        for (int w = 0; w < NW; ++w)
+            ext[w] = 0;
+        if (valid) {
+            const uint32_t ids = (uint32_t)(W[NW - 1] >> (64 - 3 * IDB));
+            const uint32_t v1 = ids & IDM, v2 = (ids >> IDB) & IDM, vt = ids >> (2 * IDB);
+            u64 arow[NW], abv[NW], a1[NW], close[NW];
+            lds_row<NW>(s_adj, vt, arow);
+            lds_row<NW>(s_above, v2, abv);
+            lds_row<NW>(s_adj, v1, a1);
+            uint32_t deg = 0;
+            bool any_close = false;
+#pragma unroll
+            for (int w = 0; w < NW; ++w) {
+                deg += __popcll(arow[w]);
+                const u64 c = arow[w] & abv[w] & ~W[w];
+                close[w] = c & a1[w];
+                ext[w] = c & ~a1[w];
+                any_close |= close[w] != 0ull;
+                nc += __popcll(ext[w]);
+                base_rec[w] = (W[w] | arow[w]) & (w == NW - 1 ? KEEP_V12 : ~0ull);  // B | N[vt]
+            }
+            uint32_t ncl = 0;
+            if (any_close && p.count) {
+#pragma unroll
+                for (int w = 0; w < NW; ++w) {
+                    u64 m = close[w];
+                    ncl += __popcll(m);
+                    while (m) {
+                        const int b = __ffsll((long long)m) - 1;
+                        m &= m - 1;
+                        hs += mix64(ks + s_key[64 * w + b]);
+                    }
+                }
+            }
+            if (child_round) {
+                n_next++;
+                cand2 += deg - 1;
+                cnt2 += ncl;
+            } else {
+                n_in++;
+                cand1 += deg - 1;
+                cnt1 += ncl;
+            }
+        }
+        // ---- push the children: on the child queue (input round) or the output queue
+        uint32_t incl = nc;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const uint32_t x = __shfl_up_sync(FULL_MASK, incl, o);
+            if (lane >= o)
+                incl += x;
+        }
+        const uint32_t T = __shfl_sync(FULL_MASK, incl, 31);
+        {
+            u64(*dst)[kQCap] = child_round ? ws.o : ws.q;
+            uint32_t pos = (child_round ? no : nq) + incl - nc;
+#pragma unroll
+            for (uint32_t c = 0; c < (uint32_t)kFMaxCh; ++c)
+                if (c < nc) {
+                    const uint32_t v = pop_lowest<NW>(ext);
+#pragma unroll
+                    for (int w = 0; w < NW - 1; ++w)
+                        dst[w][pos] = base_rec[w];
+                    dst[NW - 1][pos] = base_rec[NW - 1] | ((u64)v << (64 - IDB));
+                    dst[NW][pos] = ks + s_key[v];
+                    ++pos;
+                }
+        }
+        __syncwarp();
+        if (child_round) {
+            no += T;
+            while (no >= 32 && !out.dead)
+                flush_out(32);
+        } else {
+            nq += T;
+        }
+        if (out.dead)
+            break;
+    }
+    flush_out(no);  // the last partial group
+    // empty slots: the unused tail of the warp's last chunk
+    if (!out.dead && out.left) {
+        u64 Z[RW];
+#pragma unroll
+        for (int w = 0; w < RW; ++w)
+            Z[w] = 0;
+        for (uint32_t k = lane; k < out.left; k += 32)
+            put_record<RW, true>(out.pp, out.slot + k, log_p, Z, 0u);
+    }
+    if (!p.count)
+        cand1 = cand2 = 0;
+    Acc a;
+    a.cyc = cnt1;
+    a.hash = hs;
+    a.cand = cand1;
+    a.cyc_next = cnt2;
+    a.cand_next = cand2;
+    a.paths_next = n_next;
+    a.paths_cur = n_in;
+    a.out_real = lane == 0 ? written : 0;
+    flush<kFBlock>(a, p.sc);
+}
+
 template <int NW, bool PACK, int FUSE>
 static size_t fused_smem_t(int n)
 {
@@ -438,6 +691,9 @@ static size_t fused_smem_t(int n)
 
 size_t fused_smem(int nw, int n, bool packed, int fuse)
 {
+    if (fuse == 3)
+        return ((size_t)n * 2 * nw + ((n + 1) & ~1)) * sizeof(u64) +
+               kFWarps * (nw == 1 ? fq_warp_bytes<1>() : fq_warp_bytes<2>());
     if (nw == 1)
         return packed ? (fuse == 2 ? fused_smem_t<1, true, 2>(n) : fused_smem_t<1, true, 1>(n))
                       : (fuse == 2 ? fused_smem_t<1, false, 2>(n) : fused_smem_t<1, false, 1>(n));
@@ -449,6 +705,8 @@ typedef void (*FusedFn)(const LaunchArgs, const uint32_t);
 
 static FusedFn fused_kernel(int nw, bool pk, int fuse, bool leaf)
 {
+    if (fuse == 3)
+        return !pk || leaf ? nullptr : nw == 1 ? k_expand_fq<1> : nw == 2 ? k_expand_fq<2> : nullptr;
 #define FK(N, PK)                                                                          \
     if (nw == N && pk == PK)                                                               \
         return fuse == 2 ? k_expand_fused<N, PK, 2, false>                                 \
@@ -475,7 +733,8 @@ int fused_warps_per_launch(int nw, int n, bool packed, int fuse, bool leaf, int 
 cudaError_t launch_fused(const LaunchArgs &a, int fuse, bool leaf, uint32_t log_ch, int max_warps, cudaStream_t st)
 {
     FusedFn f = fused_kernel(a.g.nw, a.packed != 0, fuse, leaf);
-    if (!f || a.g.n > 128 || (1 << log_ch) < kFCh2 || (a.pg.log_p < log_ch) || max_warps < kFWarps)
+    // one reservation never needs more than one chunk: <= kFCh2 records (fuse 1 / 2), <= 32 (fuse 3)
+    if (!f || a.g.n > 128 || (1 << log_ch) < (fuse == 3 ? 32 : kFCh2) || (a.pg.log_p < log_ch) || max_warps < kFWarps)
         return cudaErrorInvalidValue;
     const size_t smem = fused_smem(a.g.nw, a.g.n, a.packed != 0, fuse);
     cudaError_t e = cudaFuncSetAttribute((const void *)f, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);

@@ -802,9 +802,10 @@ static cc_status enumerate_impl(const cc_graph *cg, const cc_options *opt_in, cc
                           std::getenv("CC_NO_FUSED") == nullptr;
     const u64 fused_min = std::getenv("CC_FUSED_MIN") ? std::strtoull(std::getenv("CC_FUSED_MIN"), nullptr, 10)
                                                        : (1ull << 24);
-    int fused_warps[3] = {-1, -1, -1};  // resident warps of the fused kernel: fuse 2, 1, 1 + leaf
+    const bool fq_on = !(std::getenv("CC_FQ") && std::getenv("CC_FQ")[0] == '0');
+    int fused_warps[4] = {-1, -1, -1, -1};  // resident warps of the fused kernels: fuse 2, 1, 1 + leaf, 3
     auto fwarps = [&](int fuse, bool leaf) {
-        const int i = fuse == 2 ? 0 : leaf ? 2 : 1;
+        const int i = fuse == 3 ? 3 : fuse == 2 ? 0 : leaf ? 2 : 1;
         if (fused_warps[i] < 0)
             fused_warps[i] = cc::fused_warps_per_launch(nw, (int)n, packed, fuse, leaf, sms);
         return fused_warps[i];
@@ -913,7 +914,9 @@ static cc_status enumerate_impl(const cc_graph *cg, const cc_options *opt_in, cc
         {
             // no more warps than a quarter of the free output in chunks (small arenas)
             const u64 cap_warps = std::max<u64>(8, a.out_cap / (4ull << log_ch));
-            CC_CUDA(cc::launch_fused(a, fuse, leaf, log_ch, (int)std::min<u64>((u64)fwarps(fuse, leaf), cap_warps), st));
+            // two levels on packed records: the full-round queue kernel (k_expand_fq) unless CC_FQ=0
+            const int kf = fuse == 2 && packed && fq_on ? 3 : fuse;
+            CC_CUDA(cc::launch_fused(a, kf, leaf, log_ch, (int)std::min<u64>((u64)fwarps(kf, leaf), cap_warps), st));
         }
         else if (kind == EXPAND)
             CC_CUDA(cc::launch_expand(a, mode, variant, st, grid_ex));
@@ -1213,7 +1216,8 @@ static cc_status enumerate_impl(const cc_graph *cg, const cc_options *opt_in, cc
             // output chunk of the fused kernel: about 1/64 of a warp's expected output (at least
             // 512 slots, the largest single reservation, at most 4096), so the empty slots at
             // the warps' ends stay near 1% of the launch's output
-            uint32_t log_ch = 9;
+            const bool fq = fuse == 2 && packed && fq_on;  // k_expand_fq reserves 32 slots at a time
+            uint32_t log_ch = fq ? 5 : 9;
             if (fuse) {
                 const double fe = L.fan > 0 && L.fan_fuse == fuse ? L.fan : (fuse == 2 ? est1(d) * est1(d + 1) : est1(d));
                 const double warps = std::max(1.0, std::min((double)fwarps(fuse, leaf), (double)c / 32.0));

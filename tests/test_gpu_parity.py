@@ -518,20 +518,23 @@ FUSED_GRAPHS = [("grid5x6", I.grid(5, 6), 0), ("grid6x7", I.grid(6, 7), 0), ("gr
                 ("grid6x6_k5", I.grid(6, 6), 5), ("grid6x6_k4", I.grid(6, 6), 4)]
 
 
+@pytest.mark.parametrize("fq", ["1", "0"])
 @pytest.mark.parametrize("name,g,K", FUSED_GRAPHS, ids=[x[0] for x in FUSED_GRAPHS])
-def test_fused_two_level_kernel_every_level(ws, name, g, K):
+def test_fused_two_level_kernel_every_level(ws, name, g, K, fq):
     """k_expand_fused (grid class, DESIGN.md §2 step 3d) on every level (CC_FUSED_MIN=1): two
     levels per launch, output chunks with empty slots, single-level and last-level-fusion
     launches near the cap.  Counts, hash, |F_t| and candidates equal the oracle's; the empty
-    slots never count."""
+    slots never count.  fq = 1: packed records take the full-round queue kernel k_expand_fq."""
     want = oracle.enumerate_cycles(*g, max_len=K, nthreads=NT)
     os.environ["CC_FUSED_MIN"] = "1"
     os.environ["CC_NO_SMALL"] = "1"
+    os.environ["CC_FQ"] = fq
     try:
         got = gpu(g, ws, max_len=K)
     finally:
         del os.environ["CC_FUSED_MIN"]
         del os.environ["CC_NO_SMALL"]
+        del os.environ["CC_FQ"]
     assert_same(got, want)
     s = got["stats"]
     f = got["paths_by_len"]

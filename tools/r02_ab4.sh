@@ -1,0 +1,15 @@
+#!/bin/bash
+mkdir -p gpurun_out
+python -c "from paper_1410_4876_b200 import build; build.build()" > gpurun_out/build.log 2>&1
+timeout 900 python -m pytest tests/test_gpu_parity.py -x -q -k "fused" > gpurun_out/pytest_fq.log 2>&1
+rc=$?; tail -2 gpurun_out/pytest_fq.log
+if [ $rc -ne 0 ]; then exit 1; fi
+for lib in paper_1410_4876_b200/libchordless.so variants/*.so; do
+  echo "== $lib"
+  CC_LIBCHORDLESS=$lib timeout 300 python tools/run_once.py p10x10 --repeat 3 2>&1 | python -c "
+import sys, json
+for l in sys.stdin:
+    try: d = json.loads(l); print(round(d['t_dev_ms'],1), d['hash'], d['launches'])
+    except Exception: print(l.strip()[:200])
+"
+done
