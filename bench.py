@@ -382,10 +382,11 @@ def main():
         try:
             t_ = json.load(open(tp)).get(args.workload)
             if t_:
-                recs = t_["paths_in"] + t_["children_out"]
+                recs = t_["records_levelsync"]
                 traffic = t_["dram_bytes"]
                 traffic_ratio = t_["dram_bytes"] / (recs * r_alg)
-                traffic_src = f"profiles/ncu_traffic.json ({t_['kernel']}, {t_['launch']}, {recs} records)"
+                traffic_src = (f"profiles/ncu_traffic.json ({t_['kernel']}, {t_['launch']}: {recs} records "
+                               f"level-synchronous, DRAM / moved bytes {t_['dram_over_moved']:.3f})")
         except Exception:
             traffic = traffic_ratio = traffic_src = None
     roofline = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",

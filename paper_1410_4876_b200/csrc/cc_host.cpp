@@ -856,7 +856,8 @@ static cc_status enumerate_impl(const cc_graph *cg, const cc_options *opt_in, cc
     if (const char *tp = std::getenv("CC_TRACE")) {
         trace.f = std::fopen(tp, "a");
         if (trace.f)
-            std::fprintf(trace.f, "kind,level,paths_in,children_out,cycles,candidates,ms,overflow\n");
+            std::fprintf(trace.f, "kind,level,paths_in,children_out,cycles,candidates,ms,overflow,paths_real,"
+                                  "paths_next,out_real,fuse\n");
     }
     enum Kind { STAGE1, EXPAND, FILTER };
     int trace_level = 0;
@@ -938,12 +939,14 @@ static cc_status enumerate_impl(const cc_graph *cg, const cc_options *opt_in, cc
                 S.t_expand_ms += ms;
         }
         if (trace.f)
-            std::fprintf(trace.f, "%s,%d,%llu,%llu,%llu,%llu,%.6f,%d\n",
+            std::fprintf(trace.f, "%s,%d,%llu,%llu,%llu,%llu,%.6f,%d,%llu,%llu,%llu,%d\n",
                          kind == STAGE1 ? "stage1" : kind == EXPAND ? "expand" : "filter", trace_level,
                          (unsigned long long)n_in, (unsigned long long)h_sc->out_count,
                          (unsigned long long)(h_sc->cycles + h_sc->cycles_next),
                          (unsigned long long)(h_sc->cand + h_sc->cand_next), ms,
-                         (h_sc->err || h_sc->out_count > a.out_cap) ? 1 : 0);
+                         (h_sc->err || h_sc->out_count > a.out_cap) ? 1 : 0,
+                         (unsigned long long)h_sc->paths_cur, (unsigned long long)h_sc->paths_next,
+                         (unsigned long long)h_sc->out_real, fuse);
         if (h_sc->err || h_sc->out_count > a.out_cap) {
             *overflow = true;
             if (opt.collect) {  // roll back the cycles this launch stored

@@ -1,9 +1,14 @@
 """Write profiles/ncu_traffic.json: DRAM traffic of one ncu --set full capture of the dominant
-kernel next to the algorithmic bytes of the same launch (from a CC_TRACE log of the same
-deterministic run).  bench.py reports the pair as roofline.traffic / traffic_over_alg.
+kernel next to the algorithmic bytes of the same launch (from the CC_TRACE log of the same run).
+bench.py reports the pair as roofline.traffic / traffic_over_alg.
 
-    python tools/traffic_json.py p10x10 gpurun_out/prof.ncu-rep gpurun_out/trace.csv \
-        --launch 45 --kernel 'k_expand_blocked<2,3,1,0>' --record-bytes 24
+    python tools/traffic_json.py p10x10 gpurun_out/prof44.ncu-rep gpurun_out/trace44.csv \
+        --level 44 --kernel 'k_expand_fq<2>' --record-bytes 24 --r-alg 16
+
+The captured launch is the first expansion of --level (ncu --nvtx-include "expand L<t> f<fuse>/"
+-c 1, tools/r02_prof44.sh).  Records: a two-level launch reads F_t and writes F_{t+2}; a
+level-synchronous expansion of the same paths would also write and read F_{t+1}
+(records_levelsync = in + 2 * next + out).
 """
 import argparse
 import csv
@@ -20,9 +25,10 @@ ap = argparse.ArgumentParser()
 ap.add_argument("workload")
 ap.add_argument("report")
 ap.add_argument("trace")
-ap.add_argument("--launch", type=int, required=True, help="0-based index among the expand launches")
+ap.add_argument("--level", type=int, nargs="+", required=True, help="level(s) of the captured launch")
 ap.add_argument("--kernel", required=True)
 ap.add_argument("--record-bytes", type=int, required=True)
+ap.add_argument("--r-alg", type=int, required=True, help="SURVEY 8(d) R_alg of the workload")
 a = ap.parse_args()
 
 raw = subprocess.run(["ncu", "-i", a.report, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
@@ -37,16 +43,22 @@ def metric(k):
 
 dram = metric("dram__bytes_read.sum") + metric("dram__bytes_write.sum")
 dur_ms = metric("gpu__time_duration.sum")
-expands = [r for r in csv.DictReader(open(a.trace)) if r["kind"] == "expand"]
-row = expands[a.launch]
-paths_in, out = int(row["paths_in"]), int(row["children_out"])
-alg = (paths_in + out) * a.record_bytes
+expands = [r for r in csv.DictReader(open(a.trace)) if r["kind"] == "expand" and int(r["level"]) in a.level]
+row = expands[0]
+slots_in, slots_out = int(row["paths_in"]), int(row["children_out"])
+pin, pnext, pout = int(row["paths_real"]), int(row["paths_next"]), int(row["out_real"])
+two = int(row["fuse"]) == 2
+levelsync = pin + pout + (2 * pnext if two else 0)
 path = os.path.join(ROOT, "profiles", "ncu_traffic.json")
 data = json.load(open(path)) if os.path.exists(path) else {}
 data[a.workload] = {
-    "kernel": a.kernel, "launch": f"expand launch #{a.launch + 1} (ncu -k regex:... -s {a.launch} -c 1)",
-    "paths_in": paths_in, "children_out": out, "record_bytes": a.record_bytes, "alg_bytes": alg,
-    "dram_bytes": dram, "dram_over_alg": dram / alg, "duration_ms": dur_ms,
+    "kernel": a.kernel, "launch": f"first expansion of level {row['level']} (fuse {row['fuse']})",
+    "paths_in": pin, "paths_next": pnext if two else 0, "records_out": pout,
+    "slots_in": slots_in, "slots_out": slots_out, "record_bytes": a.record_bytes,
+    "records_levelsync": levelsync, "r_alg": a.r_alg,
+    "bytes_moved": (slots_in + slots_out) * a.record_bytes, "bytes_alg": levelsync * a.r_alg,
+    "dram_bytes": dram, "dram_over_moved": dram / ((slots_in + slots_out) * a.record_bytes),
+    "dram_over_alg": dram / (levelsync * a.r_alg), "duration_ms": dur_ms,
     "source": f"{os.path.basename(a.report)} + {os.path.basename(a.trace)}",
 }
 json.dump(data, open(path, "w"), indent=1)
