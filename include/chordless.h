@@ -179,7 +179,10 @@ cc_status cc_graph_labels(const cc_graph *g, int32_t *labels);
 cc_status cc_enumerate(const cc_graph *g, const cc_options *opt, cc_result **out);
 
 /*
- * counts[k] = number of chordless cycles with exactly k vertices, k = 0..n (k < 3 is 0).
+ * counts[k] = number of chordless cycles with exactly k vertices, k = 0..n (k < 3 is 0).  A
+ * cycle's "length" is its number of vertices (= edges), the k of a k-cycle in PAPER.md:41
+ * (reading G13); Table 1 reports C3 = counts[3] and #clc = the sum
+ * over k > 3.
  * *n_lengths is always set to n+1; if cap < n+1 returns CC_ERR_BUFFER_TOO_SMALL (counts
  * untouched).  counts may be NULL with cap = 0 to query the size.  set_hash (may be NULL)
  * receives sum over cycles C of mix(sum_{v in C} key(v)) mod 2^64.

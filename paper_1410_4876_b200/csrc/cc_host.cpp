@@ -737,14 +737,17 @@ static cc_status enumerate_impl(const cc_graph *cg, const cc_options *opt_in, cc
     // ---- control block: Scratch | page table (in pages, then out pages)
     DevBuf ctrl;
     ctrl.st = st;
-    const size_t ctrl_bytes = sizeof(cc::Scratch) + (size_t)2 * npages * 4 + 256;
+    // two Scratch blocks (the second for the launch chained after Stage 1), then the page tables
+    const size_t ctrl_bytes = 2 * sizeof(cc::Scratch) + (size_t)2 * npages * 4 + 256;
     CC_CUDA(pool_alloc(&ctrl.p, ctrl_bytes, device, st));
     CC_CUDA(cudaMemsetAsync(ctrl.p, 0, sizeof(cc::Scratch), st));
     cc::Scratch *d_sc = (cc::Scratch *)ctrl.p;
-    uint32_t *d_tab = (uint32_t *)((char *)ctrl.p + sizeof(cc::Scratch));
-    CC_CUDA(t_pinned.reserve(sizeof(cc::Scratch) + (size_t)2 * npages * 4 + 64));
+    cc::Scratch *d_sc2 = d_sc + 1;
+    uint32_t *d_tab = (uint32_t *)((char *)ctrl.p + 2 * sizeof(cc::Scratch));
+    CC_CUDA(t_pinned.reserve(2 * sizeof(cc::Scratch) + (size_t)2 * npages * 4 + 64));
     cc::Scratch *h_sc = (cc::Scratch *)t_pinned.p;
-    uint32_t *h_tab = (uint32_t *)((char *)t_pinned.p + sizeof(cc::Scratch));
+    cc::Scratch *h_sc2 = h_sc + 1;
+    uint32_t *h_tab = (uint32_t *)((char *)t_pinned.p + 2 * sizeof(cc::Scratch));
 
     // ---- collect store
     if (opt.collect) {
@@ -821,19 +824,20 @@ static cc_status enumerate_impl(const cc_graph *cg, const cc_options *opt_in, cc
     const uint32_t max_len = opt.max_len;
     const bool want_paths = max_len == 0 || max_len >= 4;
 
-    cudaEvent_t ev0, ev1, ea, eb;
+    cudaEvent_t ev0, ev1, ea, eb, em;
     CC_CUDA(cudaEventCreate(&ev0));
     CC_CUDA(cudaEventCreate(&ev1));
     CC_CUDA(cudaEventCreate(&ea));
     CC_CUDA(cudaEventCreate(&eb));
+    CC_CUDA(cudaEventCreate(&em));
     struct EvGuard {
-        cudaEvent_t e[4];
+        cudaEvent_t e[5];
         ~EvGuard()
         {
             for (auto x : e)
                 cudaEventDestroy(x);
         }
-    } evg{{ev0, ev1, ea, eb}};
+    } evg{{ev0, ev1, ea, eb, em}};
     CC_CUDA(cudaEventRecord(ev0, st));
 
     u64 cyc_committed = 0;   // collect-store counter after the last committed launch
@@ -995,6 +999,151 @@ static cc_status enumerate_impl(const cc_graph *cg, const cc_options *opt_in, cc
             const u64 c = std::min<u64>(stage1_total - s1_next, (u64)free_pages.size() * P);
             if (c == 0)
                 return fail(CC_ERR_CAPACITY, "no free arena page for Stage 1");
+            // ---- Stage 1 chained with the expansion of all of F_3: both launches are queued
+            //      back to back and read back with ONE host round trip (no synchronisation in
+            //      between).  The expansion reads Stage 1's output size from the device.  Bitset
+            //      count mode outside the small-frontier path (e.g. K_{150,150}), one shard, all
+            //      pairs in one chunk.  If the expansion's output overflows, it is discarded and
+            //      F_3 continues on the ordinary path.
+            const size_t nfree0 = free_pages.size();
+            const u64 k1 = (c + P - 1) / P;
+            const int d3 = 3;
+            const bool emit3 = max_len == 0 || (u64)d3 + 1 < max_len;
+            const bool leaf3 = emit3 && max_len != 0 && (u64)d3 + 2 >= max_len;
+            const bool chain = mode == cc::Mode::B && !wide && !list && W == 1 && s1_next == 0 && c == stage1_total &&
+                               want_paths && !(small_ok && nw <= 2) && nfree0 > k1 &&
+                               std::getenv("CC_NO_CHAIN") == nullptr;
+            if (chain) {
+                for (size_t i = 0; i < nfree0; ++i)
+                    h_tab[npages + i] = free_pages[nfree0 - 1 - i];
+                CC_CUDA(cudaMemcpyAsync(d_tab + npages, h_tab + npages, nfree0 * 4, cudaMemcpyHostToDevice, st));
+                S.h2d_bytes += nfree0 * 4;
+                CC_CUDA(cudaMemsetAsync(d_sc, 0, 2 * sizeof(cc::Scratch), st));
+                cc::LaunchArgs a1 = base;
+                a1.in_lo = 0;
+                a1.n_in = c;
+                a1.out_off = 0;
+                a1.out_cap = k1 * P;
+                a1.emit = 1;
+                a1.emit_next = 1;
+                a1.count = count_tri ? 1 : 0;
+                a1.filter = 0;
+                cc::LaunchArgs a2 = base;
+                a2.sc = d_sc2;
+                a2.pg.in_pages = d_tab + npages;  // Stage 1's output pages, in table order
+                a2.n_in = 0;
+                a2.n_in_dev = &d_sc->out_count;
+                a2.out_off = k1 * P;
+                a2.out_cap = emit3 && !leaf3 ? (nfree0 - k1) * P : 0;
+                a2.emit = emit3 ? 1 : 0;
+                a2.emit_next = leaf3 ? 0 : 1;
+                a2.count = 1;
+                a2.tlen = 3;
+                if (opt.profile)
+                    CC_CUDA(cudaEventRecord(ea, st));
+                nvtxRangePushA("stage1+expand L3 chained");
+                CC_CUDA(cc::launch_stage1(a1, mode, st, grid_s1));
+                if (opt.profile)
+                    CC_CUDA(cudaEventRecord(em, st));
+                CC_CUDA(cc::launch_expand(a2, mode, variant, st, grid_ex));
+                if (opt.profile)
+                    CC_CUDA(cudaEventRecord(eb, st));
+                nvtxRangePop();
+                CC_CUDA(cudaMemcpyAsync(h_sc, d_sc, 2 * sizeof(cc::Scratch), cudaMemcpyDeviceToHost, st));
+                CC_CUDA(cudaStreamSynchronize(st));
+                S.d2h_bytes += 2 * sizeof(cc::Scratch);
+                S.launches += 2;
+                if (opt.profile) {
+                    float m1 = 0, m2 = 0;
+                    CC_CUDA(cudaEventElapsedTime(&m1, ea, em));
+                    CC_CUDA(cudaEventElapsedTime(&m2, em, eb));
+                    S.t_stage1_ms += m1;
+                    S.t_expand_ms += m2;
+                }
+                if (h_sc->err || h_sc->out_count > a1.out_cap)
+                    return fail(CC_ERR_CAPACITY, "Stage 1 output overflow (internal sizing error)");
+                const bool ok2 = !h_sc2->err && h_sc2->out_count <= a2.out_cap;
+                if (trace.f) {
+                    std::fprintf(trace.f, "stage1,2,%llu,%llu,%llu,0,0,0,0,0,%llu,0\n", (unsigned long long)c,
+                                 (unsigned long long)h_sc->out_count, (unsigned long long)h_sc->cycles,
+                                 (unsigned long long)h_sc->out_count);
+                    std::fprintf(trace.f, "expand,3,%llu,%llu,%llu,%llu,0,%d,%llu,%llu,%llu,0\n",
+                                 (unsigned long long)h_sc->out_count, (unsigned long long)h_sc2->out_count,
+                                 (unsigned long long)(h_sc2->cycles + h_sc2->cycles_next),
+                                 (unsigned long long)(h_sc2->cand + h_sc2->cand_next), ok2 ? 0 : 1,
+                                 (unsigned long long)h_sc2->paths_cur, (unsigned long long)h_sc2->paths_next,
+                                 (unsigned long long)h_sc2->out_real);
+                }
+                s1_next += c;
+                S.chunks++;
+                S.paths_written += h_sc->out_count;
+                res->counts[3] += h_sc->cycles;
+                res->hash += h_sc->hash;
+                const u64 u1 = (h_sc->out_count + P - 1) / P;
+                const u64 n3 = h_sc->out_count;
+                // pages of the table in use afterwards: F_3 (if kept) and F_4 (if expanded)
+                std::vector<char> keep(nfree0, 0);
+                Level &L3 = levels[3];
+                Level &L4 = levels[4];
+                if (ok2) {
+                    S.chunks++;
+                    S.rounds = std::max<u64>(S.rounds, 3);
+                    const u64 rin = h_sc2->paths_cur, rout = h_sc2->out_real;
+                    res->paths[3] += rin;
+                    res->cand[3] += h_sc2->cand;
+                    S.paths_expanded += rin;
+                    res->counts[4] += h_sc2->cycles;
+                    res->hash += h_sc2->hash;
+                    if (leaf3) {
+                        res->paths[4] += h_sc2->paths_next;
+                        res->cand[4] += h_sc2->cand_next;
+                        res->counts[5] += h_sc2->cycles_next;
+                        S.paths_expanded += h_sc2->paths_next;
+                        S.leaf_paths += h_sc2->paths_next;
+                    }
+                    S.paths_written += rout;
+                    S.bytes_alg += (rin + rout) * rec_bytes;
+                    S.records_levelsync += rin + rout + (leaf3 ? 2 * h_sc2->paths_next : 0);
+                    S.slots_moved += n3 + h_sc2->out_count;
+                    if (rin > 0)
+                        L3.fan1 = (double)(leaf3 ? h_sc2->paths_next : rout) / (double)rin;
+                    if (n3 > 0) {
+                        L3.fan = (double)h_sc2->out_count / (double)n3;
+                        L3.fan_fuse = 0;
+                    }
+                    const u64 u2 = (h_sc2->out_count + P - 1) / P;
+                    L4.pages.clear();
+                    for (u64 i = 0; i < u2; ++i) {
+                        keep[k1 + i] = 1;
+                        L4.pages.push_back(h_tab[npages + k1 + i]);
+                    }
+                    L4.count = h_sc2->out_count;
+                    L4.sharded = true;
+                    L4.shard_now = false;
+                    in_use += L4.count;
+                    high_water = std::max(high_water, std::max<u64>(n3, in_use));
+                    deepest = L4.count ? 4 : 2;
+                } else {
+                    L3.pages.clear();
+                    for (u64 i = 0; i < u1; ++i) {
+                        keep[i] = 1;
+                        L3.pages.push_back(h_tab[npages + i]);
+                    }
+                    L3.count = n3;
+                    L3.sharded = true;
+                    L3.shard_now = false;
+                    in_use += n3;
+                    high_water = std::max(high_water, in_use);
+                    deepest = 3;
+                }
+                // the free list keeps its pop order (table order) minus the pages kept
+                std::vector<uint32_t> nf;
+                for (size_t i = nfree0; i-- > 0;)
+                    if (!keep[i])
+                        nf.push_back(h_tab[npages + i]);
+                free_pages.swap(nf);
+                continue;
+            }
             bool of = false;
             trace_level = 2;
             cc_status s = launch(STAGE1, nullptr, 0, c, s1_next, want_paths, false, count_tri, s1_filter, used, &of);

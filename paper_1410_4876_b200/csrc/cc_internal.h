@@ -103,6 +103,8 @@ struct LaunchArgs {
     Scratch *sc;
     uint64_t in_lo;              // Stage 1 only: pair range [in_lo, in_lo + n_in)
     uint64_t n_in;               // input records (or pairs)
+    const u64 *n_in_dev;         // k_expand_blocked only: if set, the input size is read here (a
+                                 // launch chained after Stage 1 without a host round trip)
     uint64_t out_off;            // first virtual output position in out_pages
     uint64_t out_cap;            // positions available from out_off
     int32_t emit;                // 1 = create extended paths / triplets

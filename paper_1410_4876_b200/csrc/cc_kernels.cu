@@ -186,7 +186,9 @@ __global__ void __launch_bounds__(kEBBlock, NW <= 2 ? CC_EB_MINB : 2) k_expand_b
     const uint32_t idb = PACK ? p.idb : (uint32_t)kIdBits;
     const uint32_t idm = (1u << idb) - 1;
     const u64 keep_v12 = PACK ? ~((u64)idm << (64 - idb)) : ~0ull;  // packed: vt field cleared
-    const u64 n_tiles = (p.n_in + kTile - 1) / kTile;
+    // chained launch (cc_host.cpp, Stage 1 -> F_3): the input size is Stage 1's device-side count
+    const u64 n_in = p.n_in_dev ? *p.n_in_dev : p.n_in;
+    const u64 n_tiles = (n_in + kTile - 1) / kTile;
     const u64 my_tiles = blockIdx.x < n_tiles ? (n_tiles - 1 - blockIdx.x) / gridDim.x + 1 : 0;
     // tile k of this CTA -> global tile blockIdx.x + k * gridDim.x -> its page and slot
     auto issue = [&](u64 k) {
@@ -232,7 +234,7 @@ __global__ void __launch_bounds__(kEBBlock, NW <= 2 ? CC_EB_MINB : 2) k_expand_b
     for (u64 k = 0; k < my_tiles; ++k) {
         const int st = (int)(k % kStages);
         const u64 base = (blockIdx.x + k * gridDim.x) * (u64)kTile;
-        const bool full = base + kTile <= p.n_in;
+        const bool full = base + kTile <= n_in;
         mbar_wait(&bar[st], (uint32_t)((k / kStages) & 1));
         const char *buf = ring + (size_t)st * kStageBytes;
         u64 W[R][RW];
@@ -247,7 +249,7 @@ __global__ void __launch_bounds__(kEBBlock, NW <= 2 ? CC_EB_MINB : 2) k_expand_b
             id[i] = PACK ? packed_ids(W[i][NW - 1], idb) : ((const uint32_t *)(buf + (size_t)RW * kTile * 8))[j];
             // empty slots of a k_expand_fused output chunk are all-zero records: v1 == v2 == 0
             // never holds for a path (v2 = u < v1 = x, Alg. 2 l.12)
-            valid[i] = (full || base + j < p.n_in) && (id[i] & idm) != ((id[i] >> idb) & idm);
+            valid[i] = (full || base + j < n_in) && (id[i] & idm) != ((id[i] >> idb) & idm);
             paths_in += valid[i];
         }
         u64 ext[R][NW];

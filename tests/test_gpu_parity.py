@@ -597,3 +597,25 @@ def test_p8x8_collect_list_equals_oracle(ws):
     assert len(np.unique(gm)) == len(gm)  # exactly once
     assert np.array_equal(np.sort(gm), np.sort(wm))
     assert np.array_equal(np.sort(gs), np.sort(wsq))
+
+
+CHAIN_GRAPHS = [("k100x100", I.complete_bipartite(100, 100), 0), ("gnp300", I.gnp(300, 0.03, 11), 8),
+                ("grid12x12_k20", I.grid(12, 12), 20), ("grid12x12_k5", I.grid(12, 12), 5),
+                ("grid12x12_k4", I.grid(12, 12), 4), ("k60x70_k3", I.complete_bipartite(60, 70), 3)]
+
+
+@pytest.mark.parametrize("name,g,K", CHAIN_GRAPHS, ids=[x[0] for x in CHAIN_GRAPHS])
+def test_stage1_chained_with_first_expansion(ws, name, g, K):
+    """Stage 1 and the expansion of F_3 queued back to back with one host round trip (graphs
+    outside the small-frontier path): same results as the unchained path and the oracle,
+    including the last-level and no-children cases at level 3 (K = 5, 4, 3)."""
+    want = oracle.enumerate_cycles(*g, max_len=K, nthreads=NT)
+    got = gpu(g, ws, max_len=K)
+    assert_same(got, want)
+    os.environ["CC_NO_CHAIN"] = "1"
+    try:
+        plain = gpu(g, ws, max_len=K)
+    finally:
+        del os.environ["CC_NO_CHAIN"]
+    assert_same(plain, want)
+    assert got["stats"]["paths_written"] == plain["stats"]["paths_written"]
