@@ -446,15 +446,11 @@ constexpr int kQCap = 32 + kFCh1;   // child queue / output queue capacity (reco
 #endif
 constexpr int kFqStages = CC_FQ_STAGES;  // input tiles in flight per warp (cp.async ring)
 
-#ifndef CC_FQ_DIRECT
-#define CC_FQ_DIRECT 0  // 1: child rounds store F_{t+2} directly (no output queue)
-#endif
-
 template <int NW>
 struct FqWarpSmem {
     static constexpr int RW = NW + 1;
     u64 q[RW][kQCap];     // child queue (F_{t+1}), SoA
-    u64 o[RW][CC_FQ_DIRECT ? 1 : kQCap];  // output queue (F_{t+2}), SoA
+    u64 o[RW][kQCap];     // output queue (F_{t+2}), SoA
     u64 in[kFqStages][RW][32];  // input tiles, filled by cp.async (each lane copies its own record)
 };
 
@@ -637,40 +633,8 @@ __global__ void __launch_bounds__(kFBlock, CC_FUSED_MINB) k_expand_fq(const Laun
                 incl += x;
         }
         const uint32_t T = __shfl_sync(FULL_MASK, incl, 31);
-#if CC_FQ_DIRECT
-        if (child_round) {
-            // F_{t+2}: straight to this warp's output slots (consecutive per lane, the warp's
-            // records one contiguous run), no output queue
-            if (T && !out.dead) {
-                char *pp0, *pp1;
-                uint32_t s0, s1, split;
-                warp_reserve(out, T, log_ch, p, pp0, s0, pp1, s1, split);
-                if (!out.dead) {
-                    written += T;
-                    uint32_t k = incl - nc;
-#pragma unroll
-                    for (uint32_t c = 0; c < (uint32_t)kFMaxCh; ++c)
-                        if (c < nc) {
-                            const uint32_t v = pop_lowest<NW>(ext);
-                            u64 C[RW];
-#pragma unroll
-                            for (int w = 0; w < NW; ++w)
-                                C[w] = base_rec[w];
-                            C[NW - 1] |= (u64)v << (64 - IDB);
-                            C[NW] = ks + s_key[v];
-                            const bool lo = k < split;
-                            put_record<RW, true>(lo ? pp0 : pp1, lo ? s0 + k : s1 + (k - split), log_p, C, 0u);
-                            ++k;
-                        }
-                }
-            }
-            if (out.dead)
-                break;
-            continue;
-        }
-#endif
         {
-            u64(*dst)[kQCap] = child_round ? (u64(*)[kQCap])ws.o : ws.q;
+            u64(*dst)[kQCap] = child_round ? ws.o : ws.q;
             uint32_t pos = (child_round ? no : nq) + incl - nc;
 #pragma unroll
             for (uint32_t c = 0; c < (uint32_t)kFMaxCh; ++c)

@@ -1031,7 +1031,7 @@ static cc_status enumerate_impl(const cc_graph *cg, const cc_options *opt_in, cc
                 cc::LaunchArgs a2 = base;
                 a2.sc = d_sc2;
                 a2.pg.in_pages = d_tab + npages;  // Stage 1's output pages, in table order
-                a2.n_in = 0;
+                a2.n_in = c;  // an upper bound, for the grid size; the kernel reads the real count
                 a2.n_in_dev = &d_sc->out_count;
                 a2.out_off = k1 * P;
                 a2.out_cap = emit3 && !leaf3 ? (nfree0 - k1) * P : 0;
