@@ -29,6 +29,7 @@ ap.add_argument("--level", type=int, nargs="+", required=True, help="level(s) of
 ap.add_argument("--kernel", required=True)
 ap.add_argument("--record-bytes", type=int, required=True)
 ap.add_argument("--r-alg", type=int, required=True, help="SURVEY 8(d) R_alg of the workload")
+ap.add_argument("--out", default=os.path.join(ROOT, "profiles", "ncu_traffic.json"))
 a = ap.parse_args()
 
 raw = subprocess.run(["ncu", "-i", a.report, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
@@ -49,7 +50,7 @@ slots_in, slots_out = int(row["paths_in"]), int(row["children_out"])
 pin, pnext, pout = int(row["paths_real"]), int(row["paths_next"]), int(row["out_real"])
 two = int(row["fuse"]) == 2
 levelsync = pin + pout + (2 * pnext if two else 0)
-path = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+path = a.out
 data = json.load(open(path)) if os.path.exists(path) else {}
 data[a.workload] = {
     "kernel": a.kernel, "launch": f"first expansion of level {row['level']} (fuse {row['fuse']})",
