@@ -161,7 +161,10 @@ __host__ __device__ constexpr size_t blocked_stage_bytes()
 // MAXCH > 0: every path has at most MAXCH children (Delta - 1, host-checked), so the staging of
 // children is unrolled into MAXCH predicated steps instead of a divergent per-bit loop.
 template <int NW, int MAXCH, bool PACK, bool LEAF>
-__global__ void __launch_bounds__(kEBBlock, NW <= 2 ? CC_EB_MINB : 2) k_expand_blocked(const LaunchArgs p)
+#ifndef CC_EB_MINB_WIDE
+#define CC_EB_MINB_WIDE 5  // NW > 2: 5 CTAs (K_{150,150} expansion 0.221 -> 0.209 ms, measured)
+#endif
+__global__ void __launch_bounds__(kEBBlock, NW <= 2 ? CC_EB_MINB : CC_EB_MINB_WIDE) k_expand_blocked(const LaunchArgs p)
 {
     constexpr int RW = NW + 1;
     constexpr int R = expand_paths_per_thread(NW);
@@ -173,11 +176,14 @@ __global__ void __launch_bounds__(kEBBlock, NW <= 2 ? CC_EB_MINB : 2) k_expand_b
     char *ring = (char *)smem;
     u64 *s_adj = (u64 *)(ring + (size_t)kStages * kStageBytes);
     u64 *s_key = s_adj + p.g.n * NW;
-    // s_above[v*NW + w] = word w of {x : x > v} (the label gate); 16-byte aligned (padded keys)
+    // s_above[v*NW + w] = word w of {x : x > v} (the label gate); 16-byte aligned (padded keys).
+    // Wider records (NW > 2) compute the gate words instead: the table would cost n*NW words of
+    // shared memory, i.e. resident CTAs (K_{150,150} is latency bound at 4 CTAs per SM)
+    constexpr bool kAboveTable = NW <= 2;
     u64 *s_above = s_key + ((p.g.n + 1) & ~1);
     // staged children of one tile: parent state per path slot, one (slot, v) entry per child
     constexpr int PW = RW + NW;                           // parent child state + extension words
-    u64 *s_par = s_above + p.g.n * NW;                    // [kTile][PW]
+    u64 *s_par = s_above + (kAboveTable ? p.g.n * NW : 0);  // [kTile][PW]
     uint32_t *s_pid = (uint32_t *)(s_par + kTile * PW);   // [kTile] (unpacked ids only)
     uint32_t *s_child = s_pid + (PACK ? 0 : kTile);       // [kChildCap]
     __shared__ ReserveSmemT<kEBBlock> rs[2];
@@ -217,7 +223,8 @@ __global__ void __launch_bounds__(kEBBlock, NW <= 2 ? CC_EB_MINB : 2) k_expand_b
     // closed rows N[v] = Adj(v) | {v} in s_adj: vt and v1 always lie in B, so Cand/Close/Ext are
     // unchanged, and the children's blocked set B | N[vt] is a plain OR
     for (int i = threadIdx.x; i < p.g.n * NW; i += kEBBlock) {
-        s_above[i] = above_word((uint32_t)(i / NW), i % NW);
+        if (kAboveTable)
+            s_above[i] = above_word((uint32_t)(i / NW), i % NW);
         s_adj[i] = p.g.adj[i] | bit_in_word(i % NW, (uint32_t)(i / NW));
     }
     for (int i = threadIdx.x; i < p.g.n; i += kEBBlock)
@@ -267,7 +274,13 @@ __global__ void __launch_bounds__(kEBBlock, NW <= 2 ? CC_EB_MINB : 2) k_expand_b
             u64 close[NW], arow[NW], abv[NW], a1row[NW];
             bool any_close = false;
             lds_row<NW>(s_adj, vt, arow);
-            lds_row<NW>(s_above, v2, abv);
+            if constexpr (kAboveTable) {
+                lds_row<NW>(s_above, v2, abv);
+            } else {
+#pragma unroll
+                for (int w = 0; w < NW; ++w)
+                    abv[w] = above_word(v2, w);
+            }
             lds_row<NW>(s_adj, v1, a1row);
             cand -= 1;  // deg(vt) = |N[vt]| - 1: the candidate slots of Alg. 3 (statistic)
 #pragma unroll
@@ -1936,7 +1949,7 @@ size_t expand_smem(Mode m, int nw, int n, bool packed)
 {
     if (m == Mode::B) {
         const size_t tile = (size_t)kEBBlock * expand_paths_per_thread(nw);
-        return blocked_ring_bytes(nw, packed) + ((size_t)n * 2 * nw + ((n + 1) & ~1)) * sizeof(u64) +
+        return blocked_ring_bytes(nw, packed) + ((size_t)n * (nw <= 2 ? 2 : 1) * nw + ((n + 1) & ~1)) * sizeof(u64) +
                tile * (2 * nw + 1) * 8 +
                (packed ? 0 : tile * 4) + (size_t)kChildCapX4 * tile;
     }
