@@ -1959,11 +1959,13 @@ size_t expand_smem(Mode m, int nw, int n, bool packed)
 
 typedef void (*KernelFn)(const LaunchArgs);
 
+// Always raise the kernel's dynamic shared-memory limit to `smem`: the 48 KB default applies to
+// static + dynamic together, so a dynamic size just under 48 KB can still fail to launch
 static cudaError_t set_smem(KernelFn f, size_t smem)
 {
-    if (smem > 48 * 1024)
-        return cudaFuncSetAttribute((const void *)f, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    return cudaSuccess;
+    if (smem == 0)
+        return cudaSuccess;
+    return cudaFuncSetAttribute((const void *)f, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
 }
 
 static cudaError_t run(KernelFn f, unsigned int grid, size_t smem, cudaStream_t st, const LaunchArgs &a,

@@ -30,10 +30,26 @@ cases = [
     ("grid24x24 count K=13 (list class, 3 id words)", I.grid(24, 24), dict(max_len=13, record_format=2)),
     ("gnp700 count K=8 shard 1/2 (list filter)", I.gnp(700, 0.008, 11), dict(max_len=8, record_format=2, shard_index=1,
                                                                             shard_count=2, min_shard_paths=16)),
+    # round 2 kernels (environment switches force them on small graphs)
+    ("grid7x10 count (k_expand_fq, two levels, packed)", I.grid(7, 10), dict(env={"CC_FUSED_MIN": "1", "CC_NO_SMALL": "1"})),
+    ("grid7x8 count (k_expand_fused, two levels, unpacked)", I.grid(7, 8), dict(env={"CC_FUSED_MIN": "1", "CC_NO_SMALL": "1"})),
+    ("grid7x10 count K=14 (k_expand_fused, single level + leaf)", I.grid(7, 10),
+     dict(max_len=14, env={"CC_FUSED_MIN": "1", "CC_NO_SMALL": "1", "CC_FQ": "0"})),
+    ("grid7x10 count K=15 shard 1/2 (fused output with empty slots -> filter)", I.grid(7, 10),
+     dict(max_len=15, shard_index=1, shard_count=2, min_shard_paths=1 << 12, env={"CC_FUSED_MIN": "1"})),
+    ("k60x70 count (Stage 1 chained with the first expansion)", I.complete_bipartite(60, 70), {}),
+    ("p8x8 count (small-frontier kernel over page regions)", I.grid(8, 8), {}),
 ]
 bad = 0
 for name, g, kw in cases:
-    got = binding.enumerate_cycles(*g, workspace=ws, **kw)
+    kw = dict(kw)
+    env = kw.pop("env", {})
+    os.environ.update(env)
+    try:
+        got = binding.enumerate_cycles(*g, workspace=ws, **kw)
+    finally:
+        for k in env:
+            del os.environ[k]
     okw = {k: v for k, v in kw.items() if k in ("max_len", "collect")}
     if "shard_count" in kw:
         print(name, "ran; cycles on this shard:", int(got["counts"].sum()))
