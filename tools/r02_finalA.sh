@@ -12,3 +12,7 @@ done
 timeout 900 python bench.py --gpus 2 --steps 3 --warmup 3 --workspace-gb 60 --no-cpu-baseline > $O/bench_p10x10_g2.json 2> $O/bench_p10x10_g2.err
 timeout 600 python tools/run_once.py k150 --collect --repeat 2 > $O/collect_k150.log 2>&1
 ls -la $O
+timeout 900 python tools/shard_balance.py p10x10 --shards 2 4 8 > $O/shard_balance.jsonl 2> $O/shard_balance.err
+timeout 600 python tools/shard_balance.py gnp2000 --max-len 10 --shards 2 4 8 >> $O/shard_balance.jsonl 2>> $O/shard_balance.err
+timeout 600 python tools/shard_balance.py k150 --shards 2 4 8 >> $O/shard_balance.jsonl 2>> $O/shard_balance.err
+tail -c 1500 $O/shard_balance.jsonl
