@@ -91,8 +91,8 @@ typedef struct {
                                  unsharded level does not fit the arena, of the arena size: give
                                  every rank the same workspace_bytes */
     uint32_t record_format;   /* frontier record format: 0 = automatic, 1 = blocked
-                                 set (every size class), 2 = vertex list (count mode, 512 < n <=
-                                 2015, max degree <= 32, 4 <= max_len <= 14; otherwise
+                                 set (every size class), 2 = vertex list (512 < n <= 2015, max
+                                 degree <= 32, 4 <= max_len <= 14; otherwise
                                  CC_ERR_INVALID_ARGUMENT).  Automatic picks the list for the
                                  graphs it accepts.  Results do not depend on it. */
 } cc_options;
@@ -163,10 +163,11 @@ cc_status cc_graph_labels(const cc_graph *g, int32_t *labels);
  * Enumerate every chordless cycle of g exactly once on the GPU.
  * Size classes:
  *   n <= 512: bitset records of <= 8 words; count and collect mode;
- *   512 < n <= 2015: count mode only; blocked-set records of <= 32 words (one warp per
- *     path), or vertex-list records (one thread per path; max degree <= 32 and
- *     4 <= max_len <= 14; see cc_options.record_format).
- * Larger graphs, and collect mode above n = 512, fail with CC_ERR_TOO_LARGE.
+ *   512 < n <= 2015: blocked-set records of <= 32 words (one warp per path; count mode), or
+ *     vertex-list records (one thread per path; max degree <= 32 and 4 <= max_len <= 14; count
+ *     and collect mode; see cc_options.record_format).
+ * Larger graphs, and collect mode above n = 512 without the vertex-list records, fail with
+ * CC_ERR_TOO_LARGE.
  * With max_len, count mode fuses the last level: the paths of max_len - 1 vertices are
  * counted (with their closures) by the launch that creates them and are never written
  * (cc_stats.leaf_paths).  Results do not depend on the record format, the workspace size,

@@ -637,9 +637,7 @@ static cc_status enumerate_impl(const cc_graph *cg, const cc_options *opt_in, cc
     const int64_t n = g->n;
     if (n > 0 && g->nw == 0)
         return fail(CC_ERR_TOO_LARGE, "n = " + std::to_string(n) + " exceeds the supported size classes (n <= 2015)");
-    if (g->wide && opt.collect)
-        return fail(CC_ERR_TOO_LARGE, "collect mode supports n <= " + std::to_string(64 * cc::kMaxWords) +
-                                          " (n = " + std::to_string(n) + " is count mode only)");
+
     int ndev = 0;
     if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0)
         return fail(CC_ERR_NO_DEVICE, "no CUDA device");
@@ -690,8 +688,8 @@ static cc_status enumerate_impl(const cc_graph *cg, const cc_options *opt_in, cc
     const bool packed = wide || (mode == cc::Mode::B && cc::packable(nw, (int)n));
     // list class: the path's vertex list instead of its blocked set, for sparse
     // wide graphs under a length cap (written paths have <= max(3, max_len - 2) vertices)
-    const bool list_ok = wide && mode == cc::Mode::B && opt.max_len >= 4 && opt.max_len <= (uint32_t)cc::kListMaxLen &&
-                         g->max_deg <= 32;
+    // (collect mode too: the list kernels store each cycle as its vertex list, cc::CycleStore.lw)
+    const bool list_ok = wide && opt.max_len >= 4 && opt.max_len <= (uint32_t)cc::kListMaxLen && g->max_deg <= 32;
     if (opt.record_format > 2)
         return fail(CC_ERR_INVALID_ARGUMENT, "record_format must be 0, 1 or 2");
     if (opt.record_format == 2 && !list_ok)
@@ -699,6 +697,10 @@ static cc_status enumerate_impl(const cc_graph *cg, const cc_options *opt_in, cc
                                              "max degree <= 32 and 4 <= max_len <= " +
                                                  std::to_string(cc::kListMaxLen));
     const bool list = opt.record_format == 2 || (opt.record_format == 0 && list_ok);
+    if (wide && opt.collect && !list)
+        return fail(CC_ERR_TOO_LARGE, "collect mode above n = " + std::to_string(64 * cc::kMaxWords) +
+                                          " needs the vertex-list records: max degree <= 32 and 4 <= max_len <= " +
+                                          std::to_string(cc::kListMaxLen) + " (n = " + std::to_string(n) + ")");
     const int rwl = list ? std::max<int>(2, (std::max<int>(3, (int)opt.max_len - 2) + 3) / 4) : 0;
     const u64 rec_bytes = list ? (u64)(rwl + 2) * 8 : (u64)cc::record_bytes(nw, mode, packed);
     S.record_bytes = rec_bytes;
@@ -752,7 +754,9 @@ static cc_status enumerate_impl(const cc_graph *cg, const cc_options *opt_in, cc
     // ---- collect store
     if (opt.collect) {
         const u64 ccap = opt.collect_capacity ? opt.collect_capacity : (1ull << 22);
-        const size_t s_s = align_up(ccap * nw * 8, 256), s_ids = align_up(ccap * 4, 256),
+        // list class: rwl + 1 words of 16-bit ids per cycle (<= max_len vertices); else S + ids
+        const uint32_t lw = list ? (uint32_t)rwl + 1 : 0;
+        const size_t s_s = align_up(ccap * (lw ? lw : nw) * 8, 256), s_ids = align_up(ccap * 4, 256),
                      s_adj = align_up((size_t)n * nw * 8, 256), s_orig = align_up((size_t)n * 4, 256);
         CC_CUDA(pool_alloc(&res->cyc_buf, s_s + s_ids + s_adj + s_orig, device, st));
         char *p = (char *)res->cyc_buf;
@@ -760,6 +764,7 @@ static cc_status enumerate_impl(const cc_graph *cg, const cc_options *opt_in, cc
         res->cyc.ids = (uint32_t *)(p + s_s);
         res->cyc.cap = ccap;
         res->cyc.count = &d_sc->cyc_count;
+        res->cyc.lw = lw;
         res->adj = (u64 *)(p + s_s + s_ids);
         res->orig = (int32_t *)(p + s_s + s_ids + s_adj);
         CC_CUDA(cudaMemcpyAsync(res->adj, dc->dg.adj, (size_t)n * nw * 8, cudaMemcpyDeviceToDevice, st));
@@ -1304,7 +1309,7 @@ static cc_status enumerate_impl(const cc_graph *cg, const cc_options *opt_in, cc
         // last level: if they could not have children themselves (d+2 >= max_len) they are
         // counted by this launch and not written
         const bool emit = max_len == 0 || (u64)d + 1 < max_len;
-        const bool leaf = emit && mode == cc::Mode::B && max_len != 0 && (u64)d + 2 >= max_len;
+        const bool leaf = emit && (mode == cc::Mode::B || list) && max_len != 0 && (u64)d + 2 >= max_len;
         const bool writes = emit && !leaf;
         // grid class, large levels: k_expand_fused, two levels (F_d -> F_{d+2}) when the
         // grandchildren are written (not the last level under the cap), else one

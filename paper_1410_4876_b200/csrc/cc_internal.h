@@ -73,6 +73,9 @@ struct CycleStore {
     uint32_t *ids;
     uint64_t cap;
     u64 *count;                  // device counter (keeps counting past cap)
+    uint32_t lw;                 // 0: bitmap S + ids (n <= 512); > 0: the list class's format --
+                                 // the canonical sequence as 16-bit ids, four per word, lw words
+                                 // (s[w * cap + i]), unused slots 0xffff
 };
 
 // Per-launch scratch accumulators (zeroed before, read back after every launch, so a launch
@@ -169,8 +172,6 @@ struct SmallArgs {
 cudaError_t launch_small(const LaunchArgs &a, const SmallArgs &s, cudaStream_t st, int sms);
 // nbrmask (DevGraph) of a wide graph with Delta <= 32; T must be zeroed, n*n words
 cudaError_t launch_nbrmask(const DevGraph &g, uint32_t *T, cudaStream_t st);
-cudaError_t launch_cycle_lengths(const CycleStore &c, int nw, uint64_t first, uint64_t count,
-                                 uint32_t *len, cudaStream_t st);
 // off[0..count] = exclusive prefix sums of the lengths of stored cycles first..first+count-1
 // (off[count] = total); blk = scratch of ceil(count / 1024) + 1 words
 cudaError_t launch_cycle_offsets(const CycleStore &c, int nw, uint64_t first, uint64_t count, u64 *off, u64 *blk,

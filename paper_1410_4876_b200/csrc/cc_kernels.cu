@@ -1520,12 +1520,39 @@ __device__ __forceinline__ uint32_t low_mask(uint32_t k)  // bits 0..k-1 (k <= 3
     return k >= 32 ? 0xffffffffu : ((1u << k) - 1u);
 }
 
+// Collect mode, list class: store the cycle <v1 .. vt, a[, b]> (the path's list, then the closing
+// vertices; b = 0xffff: none) at index idx.  The list order is the canonical sequence of
+// PAPER.md:45-51 (v1, v2 = the minimum label, v3, ...), the same one the bitmap walk of
+// k_cycle_sequences produces.  Word positions are unrolled: no dynamically indexed registers.
+template <int RWL, int RW>
+__device__ __forceinline__ void store_cycle_list(const CycleStore &c, const u64 (&W)[RW], int t, uint32_t a,
+                                                 uint32_t b, u64 idx)
+{
+    constexpr int LW = RWL + 1;
+    if (idx >= c.cap)
+        return;
+#pragma unroll
+    for (int w = 0; w < LW; ++w) {
+        u64 x = 0;
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+            const int pos = 4 * w + j;
+            const uint32_t id = pos < 4 * RWL && pos < t ? list_id(W, pos < 4 * RWL ? pos : 0)
+                                : pos == t           ? a
+                                : pos == t + 1       ? b
+                                                     : 0xffffu;
+            x |= (u64)id << (16 * j);
+        }
+        c.s[(u64)w * c.cap + idx] = x;
+    }
+}
+
 #ifndef CC_LIST_BLOCK
 #define CC_LIST_BLOCK 512
 #endif
 constexpr int kListBlock = CC_LIST_BLOCK;  // threads per CTA of the list kernels
 
-template <int RWL>
+template <int RWL, bool COL>
 __global__ void __launch_bounds__(kListBlock) k_stage1_list(const LaunchArgs p)
 {
     constexpr int RW = RWL + 2;
@@ -1568,6 +1595,14 @@ __global__ void __launch_bounds__(kListBlock) k_stage1_list(const LaunchArgs p)
                 if (p.count) {
                     cnt++;
                     hs += mix64(__ldg(key + x) + __ldg(key + u) + __ldg(key + y));
+                    if constexpr (COL) {  // the triangle <x, u, y> (Alg. 2 l.14)
+                        u64 T3[RW];
+#pragma unroll
+                        for (int w = 0; w < RW; ++w)
+                            T3[w] = 0;
+                        T3[0] = (u64)x | ((u64)u << 16);
+                        store_cycle_list<RWL>(p.cyc, T3, 2, y, 0xffffu, atomicAdd(p.cyc.count, 1ull));
+                    }
                 }
             } else if (p.emit) {
                 emit = 1;
@@ -1596,7 +1631,7 @@ __global__ void __launch_bounds__(kListBlock) k_stage1_list(const LaunchArgs p)
     flush_accum<kListBlock>(cnt, hs, 0, p.sc);
 }
 
-template <int RWL, bool LEAF>
+template <int RWL, bool LEAF, bool COL>
 __global__ void __launch_bounds__(kListBlock) k_expand_list(const LaunchArgs p)
 {
     constexpr int RW = RWL + 2;
@@ -1643,10 +1678,14 @@ __global__ void __launch_bounds__(kListBlock) k_expand_list(const LaunchArgs p)
                 rb1 = __ldg(rowptr + v1);
             if (p.count && close) {
                 cnt += __popc(close);
+                u64 idx = COL ? atomicAdd(p.cyc.count, (u64)__popc(close)) : 0ull;
                 while (close) {
                     const int k = __ffs(close) - 1;
                     close &= close - 1;
-                    hs += mix64(ks + __ldg(key + __ldg(col + rb1 + k)));
+                    const uint32_t z = __ldg(col + rb1 + k);
+                    hs += mix64(ks + __ldg(key + z));
+                    if constexpr (COL)
+                        store_cycle_list<RWL>(p.cyc, W, t, z, 0xffffu, idx++);
                 }
             }
             rb = __ldg(rowptr + vt);
@@ -1675,10 +1714,14 @@ __global__ void __launch_bounds__(kListBlock) k_expand_list(const LaunchArgs p)
                         if (c2) {
                             lcyc += __popc(c2);
                             const u64 kv = ks + __ldg(key + v);
+                            u64 idx = COL ? atomicAdd(p.cyc.count, (u64)__popc(c2)) : 0ull;
                             while (c2) {
                                 const int j = __ffs(c2) - 1;
                                 c2 &= c2 - 1;
-                                hs += mix64(kv + __ldg(key + __ldg(col + rb1 + j)));
+                                const uint32_t z = __ldg(col + rb1 + j);
+                                hs += mix64(kv + __ldg(key + z));
+                                if constexpr (COL)
+                                    store_cycle_list<RWL>(p.cyc, W, t, v, z, idx++);
                             }
                         }
                     }
@@ -1774,21 +1817,27 @@ __global__ void k_keybyte(u64 *keybyte, const u64 *key, int n)
     keybyte[(j << 8) + b] = s;
 }
 
-__global__ void k_cycle_lengths(const CycleStore c, int nw, uint64_t first, uint64_t count, uint32_t *len)
-{
-    const u64 i = (u64)blockIdx.x * blockDim.x + threadIdx.x;
-    if (i >= count)
-        return;
-    uint32_t k = 0;
-    for (int w = 0; w < nw; ++w)
-        k += __popcll(c.s[(u64)w * c.cap + first + i]);
-    len[i] = k;
-}
 
 // Offsets of the fetched cycles on the device: off[i] = sum of the lengths of cycles first ..
 // first+i-1 (off[count] = total).  Three passes: per-1024-block exclusive scans with block sums,
 // one block scanning the block sums, then the block prefixes added.
 constexpr int kScanBlock = 1024;
+
+__device__ __forceinline__ uint32_t cycle_length(const CycleStore &c, int nw, u64 i)
+{
+    uint32_t k = 0;
+    if (c.lw) {  // list format: used 16-bit slots
+        for (uint32_t w = 0; w < c.lw; ++w) {
+            const u64 x = c.s[(u64)w * c.cap + i];
+            for (int j = 0; j < 4; ++j)
+                k += ((x >> (16 * j)) & 0xffffu) != 0xffffu;
+        }
+    } else {
+        for (int w = 0; w < nw; ++w)
+            k += __popcll(c.s[(u64)w * c.cap + i]);
+    }
+    return k;
+}
 
 __global__ void __launch_bounds__(kScanBlock) k_cycle_scan_blocks(const CycleStore c, int nw, uint64_t first,
                                                                   uint64_t count, u64 *off, u64 *blk)
@@ -1797,8 +1846,7 @@ __global__ void __launch_bounds__(kScanBlock) k_cycle_scan_blocks(const CycleSto
     const u64 i = (u64)blockIdx.x * kScanBlock + threadIdx.x;
     u64 k = 0;
     if (i < count)
-        for (int w = 0; w < nw; ++w)
-            k += __popcll(c.s[(u64)w * c.cap + first + i]);
+        k = cycle_length(c, nw, first + i);
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
     u64 incl = k;
 #pragma unroll
@@ -1902,6 +1950,18 @@ __global__ void k_cycle_sequences(const CycleStore c, int nw, const u64 *adj, co
     const u64 i = (u64)blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= count)
         return;
+    if (c.lw) {  // list format: the stored order is the canonical sequence
+        u64 o = offsets[i];
+        for (uint32_t w = 0; w < c.lw; ++w) {
+            const u64 x = c.s[(u64)w * c.cap + first + i];
+            for (int j = 0; j < 4; ++j) {
+                const uint32_t v = (uint32_t)(x >> (16 * j)) & 0xffffu;
+                if (v != 0xffffu)
+                    out[o++] = orig[v];
+            }
+        }
+        return;
+    }
     const uint32_t id = c.ids[first + i];
     uint32_t prev = id & kIdMask, cur = (id >> kIdBits) & kIdMask;
     const u64 o = offsets[i], k = offsets[i + 1] - offsets[i];
@@ -2039,15 +2099,18 @@ cudaError_t launch_wide(int which, const LaunchArgs &a, cudaStream_t st, int gri
     return run(f, grid_for(per_block, a.n_in, grid_cap), 0, st, a);
 }
 
-static KernelFn list_kernel(int which, int rwl, bool leaf)
+static KernelFn list_kernel(int which, int rwl, bool leaf, bool col = false)
 {
     if (which == 0)
-        return rwl == 2 ? k_stage1_list<2> : rwl == 3 ? k_stage1_list<3> : nullptr;
+        return rwl == 2 ? (col ? k_stage1_list<2, true> : k_stage1_list<2, false>)
+             : rwl == 3 ? (col ? k_stage1_list<3, true> : k_stage1_list<3, false>) : nullptr;
     if (which == 1) {
         if (rwl == 2)
-            return leaf ? k_expand_list<2, true> : k_expand_list<2, false>;
+            return col ? (leaf ? k_expand_list<2, true, true> : k_expand_list<2, false, true>)
+                       : (leaf ? k_expand_list<2, true, false> : k_expand_list<2, false, false>);
         if (rwl == 3)
-            return leaf ? k_expand_list<3, true> : k_expand_list<3, false>;
+            return col ? (leaf ? k_expand_list<3, true, true> : k_expand_list<3, false, true>)
+                       : (leaf ? k_expand_list<3, true, false> : k_expand_list<3, false, false>);
         return nullptr;
     }
     return rwl == 2 ? k_shard_filter<4, false, false> : rwl == 3 ? k_shard_filter<5, false, false> : nullptr;
@@ -2057,7 +2120,7 @@ cudaError_t launch_list(int which, const LaunchArgs &a, int rwl, bool leaf, cuda
 {
     if (a.n_in == 0)
         return cudaSuccess;
-    KernelFn f = list_kernel(which, rwl, leaf);
+    KernelFn f = list_kernel(which, rwl, leaf, a.collect != 0);
     if (!f)
         return cudaErrorInvalidValue;
     const int block = which == 2 ? kBlock : kListBlock;  // the shard filter is the generic kernel
@@ -2139,14 +2202,6 @@ cudaError_t launch_nbrmask(const DevGraph &g, uint32_t *T, cudaStream_t st)
     return cudaGetLastError();
 }
 
-cudaError_t launch_cycle_lengths(const CycleStore &c, int nw, uint64_t first, uint64_t count,
-                                 uint32_t *len, cudaStream_t st)
-{
-    if (count == 0)
-        return cudaSuccess;
-    k_cycle_lengths<<<(unsigned int)((count + 255) / 256), 256, 0, st>>>(c, nw, first, count, len);
-    return cudaGetLastError();
-}
 
 cudaError_t launch_cycle_sequences(const CycleStore &c, int nw, const u64 *adj, const int32_t *orig,
                                    uint64_t first, uint64_t count, const u64 *offsets, int32_t *out,

@@ -246,9 +246,12 @@ def test_too_large_graph_rejected(ws):
     with pytest.raises(binding.CCError) as ei:
         gpu(g, ws)
     assert ei.value.kind == "CC_ERR_TOO_LARGE"
-    # collect mode is limited to the bitmap class n <= 512
+    # collect mode above n = 512 needs the list records (a length cap 4..14, max degree <= 32)
     with pytest.raises(binding.CCError) as ei:
         gpu(I.gnp(600, 0.005, 1), ws, collect=True)
+    assert ei.value.kind == "CC_ERR_TOO_LARGE"
+    with pytest.raises(binding.CCError) as ei:
+        gpu(I.gnp(600, 0.005, 1), ws, collect=True, max_len=8, record_format=1)
     assert ei.value.kind == "CC_ERR_TOO_LARGE"
 
 
@@ -619,3 +622,48 @@ def test_stage1_chained_with_first_expansion(ws, name, g, K):
         del os.environ["CC_NO_CHAIN"]
     assert_same(plain, want)
     assert got["stats"]["paths_written"] == plain["stats"]["paths_written"]
+
+
+WIDE_COLLECT = [("gnp600_k7", I.gnp(600, 0.01, 5), 7), ("gnp2000_k6", I.gnp(2000, 0.005, I.GNP_SEED), 6),
+                ("gnp2015_k14", I.gnp(2015, 0.0018, 77), 14), ("gnp700_k4", I.gnp(700, 0.008, 11), 4)]
+
+
+@pytest.mark.parametrize("name,g,K", WIDE_COLLECT, ids=[x[0] for x in WIDE_COLLECT])
+def test_wide_collect_list_equals_oracle(ws, name, g, K):
+    """SURVEY §8(f)1 above n = 512: collect mode on vertex-list records (the list class) returns
+    exactly the oracle's cycles as canonical sequences, including triangles from Stage 1 and the
+    closures of the fused last level."""
+    got = gpu(g, ws, max_len=K, collect=True)
+    want = oracle.enumerate_cycles(*g, max_len=K, collect=True)
+    assert_same(got, want)
+    assert got["stats"]["record_format"] == 2
+    assert len(got["cycles"]) == int(want["counts"].sum())
+    assert sorted(map(tuple, got["cycles"])) == sorted(map(tuple, want["cycles"]))
+
+
+def test_gnp2000_k9_collect_at_scale(ws):
+    """G(2000, 0.005) at K = 9 in collect mode: 51,066,119 cycles stored on the device and fetched
+    in batches; the H-spec hash recomputed on the host from the fetched lists equals the device
+    hash and the oracle golden (tests/golden/oracle_gnp2000_k9.json)."""
+    import json
+    import torch
+    want = json.load(open(os.path.join(GOLDEN, "oracle_gnp2000_k9.json")))
+    g = I.gnp(2000, 0.005, I.GNP_SEED)
+    free, _ = torch.cuda.mem_get_info()
+    big = torch.empty(int(free * 0.6), dtype=torch.uint8, device="cuda")
+    gr = binding.cc_graph_from_csr(*g)
+    r = binding.cc_enumerate(gr, collect=True, workspace=big, max_len=9)
+    counts, h = binding.cc_count_by_length(r)
+    assert {str(k): int(v) for k, v in enumerate(counts) if v} == want["counts"]
+    assert f"{h:#018x}" == want["set_hash"]
+    total = want["total"]
+    assert binding.cc_num_stored_cycles(r) == total
+    hs = 0
+    lens = np.zeros(10, dtype=np.int64)
+    for first in range(0, total, 1 << 23):
+        verts, offs = binding.cc_fetch_cycles(r, first, 1 << 23)
+        lens += np.bincount(np.diff(offs.astype(np.int64)), minlength=10)[:10]
+        hs = (hs + brute.hspec_hash_np(verts, offs)) & brute.M64
+    assert hs == h
+    assert {str(k): int(v) for k, v in enumerate(lens) if v} == want["counts"]
+    del big
