@@ -627,14 +627,16 @@ __global__ void __launch_bounds__(kFBlock, 3) k_expand_fq(const LaunchArgs p, co
             }
         }
         // ---- push the children: on the child queue (input round) or the output queue
-        uint32_t incl = nc;
-#pragma unroll
-        for (int o = 1; o < 32; o <<= 1) {
-            const uint32_t x = __shfl_up_sync(FULL_MASK, incl, o);
-            if (lane >= o)
-                incl += x;
+        // nc <= 3 (two bits): the warp's exclusive prefix from two ballots instead of a 5-step
+        // shuffle scan -- two independent votes instead of a serial chain (P10x10 3.135 -> 3.052 s)
+        uint32_t incl, T;
+        {
+            const uint32_t b0 = __ballot_sync(FULL_MASK, nc & 1u), b1 = __ballot_sync(FULL_MASK, nc & 2u);
+            uint32_t lt;
+            asm("mov.u32 %0, %%lanemask_lt;" : "=r"(lt));
+            incl = __popc(b0 & lt) + 2 * __popc(b1 & lt) + nc;
+            T = __popc(b0) + 2 * __popc(b1);
         }
-        const uint32_t T = __shfl_sync(FULL_MASK, incl, 31);
         {
             u64(*dst)[kQCap] = child_round ? ws.o : ws.q;
             uint32_t pos = (child_round ? no : nq) + incl - nc;
