@@ -56,7 +56,9 @@ typedef struct {
     uint32_t struct_size;     /* = sizeof(cc_options); ABI versioning */
     int32_t device;           /* CUDA ordinal; -1 = the calling thread's current device */
     void *stream;             /* cudaStream_t to run on (e.g. torch's current stream);
-                                 NULL = the legacy default stream */
+                                 NULL = the legacy default stream.  cc_fetch_cycles and
+                                 cc_result_free of the result also run on it: it must stay valid
+                                 until the result is freed */
     uint32_t max_len;         /* 0 = no cap; else only cycles with <= max_len vertices are
                                  enumerated and counted (reading G14) */
     uint32_t collect;         /* 0 = counts + set hash only (the paper's count-only mode,
