@@ -445,6 +445,26 @@ constexpr int kQCap = 32 + kFCh1;   // child queue / output queue capacity (reco
 #define CC_FQ_STAGES 2
 #endif
 constexpr int kFqStages = CC_FQ_STAGES;  // input tiles in flight per warp (cp.async ring)
+#ifndef CC_FQ_CONTIG
+#define CC_FQ_CONTIG 1  // each warp reads a contiguous share of the input level
+#endif
+#ifndef CC_FQ_GATHER
+#define CC_FQ_GATHER 1  // children from a byte gather over vt's neighbour slots (NbrSlots)
+#endif
+
+// Neighbour slots of a vertex v (max degree <= 4), for the byte gather of the extension set.
+// Every child of a path ending in v is a neighbour of v, so the <= 3 set bits of Ext (an
+// NW-word set) lie in the bytes that hold v's neighbours u_0 < u_1 < ... (CSR order).  Two
+// byte permutes move byte u_k >> 3 of Ext into byte k of one 32-bit word, a mask keeps bit
+// u_k & 7 of it:  g = (prmt(e0, e1, sel_lo) & m_lo) | (prmt(e2, e3, sel_hi) & m_hi), where
+// e0..e3 are the 32-bit quarters of Ext and (lo, hi) the slots whose byte is in bytes 0-7 /
+// 8-15.  Bit 8k + (u_k & 7) of g is set iff u_k is a child; the child's vertex is byte k of nb.
+struct NbrSlots {
+    uint32_t sel;    // low 16 bits: prmt selector over (e0, e1); high 16 bits: over (e2, e3)
+    uint32_t m_lo;   // mask of the slots read from bytes 0-7
+    uint32_t m_hi;   // mask of the slots read from bytes 8-15
+    uint32_t nb;     // byte k = u_k
+};
 
 template <int NW>
 struct FqWarpSmem {
@@ -483,14 +503,33 @@ __global__ void __launch_bounds__(kFBlock, 3) k_expand_fq(const LaunchArgs p, co
     u64 *s_adj = smem;                          // closed rows N[v] = Adj(v) | {v}
     u64 *s_above = s_adj + n * NW;              // label gate {x : x > v}
     u64 *s_key = s_above + n * NW;              // key(v)
-    char *wbase = (char *)(s_key + ((n + 1) & ~1));
+    NbrSlots *s_nbx = (NbrSlots *)(s_key + ((n + 1) & ~1));  // neighbour slots (CC_FQ_GATHER)
+    char *wbase = (char *)(s_nbx + (CC_FQ_GATHER ? ((n + 1) & ~1) : 0));
     WS &ws = *(WS *)(wbase + (threadIdx.x >> 5) * fq_warp_bytes<NW>());
     for (int i = threadIdx.x; i < n * NW; i += kFBlock) {
         s_above[i] = above_word((uint32_t)(i / NW), i % NW);
         s_adj[i] = p.g.adj[i] | bit_in_word(i % NW, (uint32_t)(i / NW));
     }
-    for (int i = threadIdx.x; i < n; i += kFBlock)
+    for (int i = threadIdx.x; i < n; i += kFBlock) {
         s_key[i] = p.g.key[i];
+#if CC_FQ_GATHER
+        NbrSlots e{0u, 0u, 0u, 0u};
+        const uint32_t r0 = p.g.rowptr[i], d = p.g.rowptr[i + 1] - r0;  // d <= 4 (host: max_deg)
+        for (uint32_t k = 0; k < d; ++k) {
+            const uint32_t u = p.g.col[r0 + k], byte = u >> 3;
+            const uint32_t bit = 1u << (8 * k + (u & 7));
+            e.nb |= u << (8 * k);
+            if (byte < 8) {
+                e.sel |= byte << (4 * k);
+                e.m_lo |= bit;
+            } else {
+                e.sel |= (byte - 8) << (16 + 4 * k);
+                e.m_hi |= bit;
+            }
+        }
+        s_nbx[i] = e;
+#endif
+    }
     __syncthreads();
 
     const int lane = threadIdx.x & 31;
@@ -502,6 +541,35 @@ __global__ void __launch_bounds__(kFBlock, 3) k_expand_fq(const LaunchArgs p, co
     u64 hs = 0;
     uint32_t nq = 0, no = 0;  // warp-uniform queue fills
 
+#if CC_FQ_CONTIG
+    // input tile k of this warp = tile t_beg + k of its contiguous share [t_beg, t_end) of the
+    // level (static split: every tile holds 32 paths of about the same expected work); the page
+    // pointer is looked up only when the share crosses a page (tiles never straddle pages)
+    const u64 gw = blockIdx.x * (u64)kFWarps + (threadIdx.x >> 5);
+    const u64 t_beg = nt * gw / tw, t_end = nt * (gw + 1) / tw;
+    const uint32_t tsh = log_p - 5;  // tiles per page = 2^tsh
+    uint32_t cur_pg = ~0u;
+    const char *cur_pp = nullptr;
+    auto issue = [&](u64 k) {
+        const u64 t = t_beg + k;
+        if (t < t_end) {
+            const uint32_t pg = (uint32_t)(t >> tsh);
+            if (pg != cur_pg) {
+                cur_pg = pg;
+                cur_pp = page_ptr(p.pg, p.pg.in_pages[pg]);
+            }
+            const uint32_t slot = (((uint32_t)t << 5) & ((1u << log_p) - 1)) + lane;
+            const u64 *src = (const u64 *)cur_pp + slot;
+            const int stg = (int)(k % kFqStages);
+#pragma unroll
+            for (int w = 0; w < RW; ++w)
+                cp_async8(&ws.in[stg][w][lane], src + ((u64)w << log_p));
+        }
+        cp_async_commit();
+    };
+    auto tile_of = [&](u64 k) { return t_beg + k; };
+    auto more_in = [&](u64 k) { return t_beg + k < t_end; };
+#else
     // input tile k of this warp (global tile wt0 + k * tw) -> ring stage k % kFqStages; one
     // commit group per tile, empty groups past the end keep the wait counts uniform
     const u64 wt0 = blockIdx.x * (u64)kFWarps + (threadIdx.x >> 5);
@@ -518,6 +586,9 @@ __global__ void __launch_bounds__(kFBlock, 3) k_expand_fq(const LaunchArgs p, co
         }
         cp_async_commit();
     };
+    auto tile_of = [&](u64 k) { return wt0 + k * tw; };
+    auto more_in = [&](u64 k) { return wt0 + k * tw < nt; };
+#endif
     // write the 32 (or, at the end, fewer) records at the end of the output queue
     auto flush_out = [&](uint32_t T) {
         if (T == 0 || out.dead)
@@ -542,7 +613,7 @@ __global__ void __launch_bounds__(kFBlock, 3) k_expand_fq(const LaunchArgs p, co
 
     u64 W[RW];
     u64 kin = 0;  // next input tile of this warp
-    bool have_in = wt0 < nt;
+    bool have_in = more_in(0);
 #pragma unroll
     for (int k = 0; k < kFqStages - 1; ++k)
         issue((u64)k);
@@ -567,10 +638,10 @@ __global__ void __launch_bounds__(kFBlock, 3) k_expand_fq(const LaunchArgs p, co
 #pragma unroll
             for (int w = 0; w < RW; ++w)
                 W[w] = ws.in[stg][w][lane];
-            const u64 r = ((wt0 + kin * tw) << 5) + lane;
+            const u64 r = (tile_of(kin) << 5) + lane;
             issue(kin + kFqStages - 1);  // refill the stage read a round ago
             ++kin;
-            have_in = wt0 + kin * tw < nt;
+            have_in = more_in(kin);
             const uint32_t ids = (uint32_t)(W[NW - 1] >> (64 - 3 * IDB));
             valid = r < p.n_in && (ids & IDM) != ((ids >> IDB) & IDM);  // empty slot: v1 == v2
         } else {
@@ -584,6 +655,9 @@ __global__ void __launch_bounds__(kFBlock, 3) k_expand_fq(const LaunchArgs p, co
 #pragma unroll
         for (int w = 0; w < NW; ++w)
             ext[w] = 0;
+#if CC_FQ_GATHER
+        uint32_t gch = 0, gnb = 0;  // children as bits of the slot gather, vt's neighbour bytes
+#endif
         if (valid) {
             const uint32_t ids = (uint32_t)(W[NW - 1] >> (64 - 3 * IDB));
             const uint32_t v1 = ids & IDM, v2 = (ids >> IDB) & IDM, vt = ids >> (2 * IDB);
@@ -593,16 +667,31 @@ __global__ void __launch_bounds__(kFBlock, 3) k_expand_fq(const LaunchArgs p, co
             lds_row<NW>(s_adj, v1, a1);
             uint32_t deg = 0;
             bool any_close = false;
+#if CC_FQ_GATHER
+            const NbrSlots e = s_nbx[vt];
+            deg = __popc(e.m_lo | e.m_hi) + 1;  // |N[vt]|: one mask bit per neighbour
+#endif
 #pragma unroll
             for (int w = 0; w < NW; ++w) {
+#if !CC_FQ_GATHER
                 deg += __popcll(arow[w]);
+#endif
                 const u64 c = arow[w] & abv[w] & ~W[w];
                 close[w] = c & a1[w];
                 ext[w] = c & ~a1[w];
                 any_close |= close[w] != 0ull;
+#if !CC_FQ_GATHER
                 nc += __popcll(ext[w]);
+#endif
                 base_rec[w] = (W[w] | arow[w]) & (w == NW - 1 ? KEEP_V12 : ~0ull);  // B | N[vt]
             }
+#if CC_FQ_GATHER
+            gch = __byte_perm((uint32_t)ext[0], (uint32_t)(ext[0] >> 32), e.sel & 0xffffu) & e.m_lo;
+            if constexpr (NW == 2)
+                gch |= __byte_perm((uint32_t)ext[1], (uint32_t)(ext[1] >> 32), e.sel >> 16) & e.m_hi;
+            gnb = e.nb;
+            nc = __popc(gch);
+#endif
             uint32_t ncl = 0;
             if (any_close && p.count) {
 #pragma unroll
@@ -643,7 +732,13 @@ __global__ void __launch_bounds__(kFBlock, 3) k_expand_fq(const LaunchArgs p, co
 #pragma unroll
             for (uint32_t c = 0; c < (uint32_t)kFMaxCh; ++c)
                 if (c < nc) {
+#if CC_FQ_GATHER
+                    const uint32_t b = 31u - __clz(gch);  // highest slot bit
+                    gch ^= 1u << b;
+                    const uint32_t v = __byte_perm(gnb, 0u, 0x4440u | (b >> 3));
+#else
                     const uint32_t v = pop_lowest<NW>(ext);
+#endif
 #pragma unroll
                     for (int w = 0; w < NW - 1; ++w)
                         dst[w][pos] = base_rec[w];
@@ -697,6 +792,7 @@ size_t fused_smem(int nw, int n, bool packed, int fuse)
 {
     if (fuse == 3)
         return ((size_t)n * 2 * nw + ((n + 1) & ~1)) * sizeof(u64) +
+               (CC_FQ_GATHER ? ((size_t)(n + 1) & ~(size_t)1) * sizeof(NbrSlots) : 0) +
                kFWarps * (nw == 1 ? fq_warp_bytes<1>() : fq_warp_bytes<2>());
     if (nw == 1)
         return packed ? (fuse == 2 ? fused_smem_t<1, true, 2>(n) : fused_smem_t<1, true, 1>(n))
