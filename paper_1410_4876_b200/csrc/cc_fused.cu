@@ -445,8 +445,8 @@ constexpr int kQCap = 32 + kFCh1;   // child queue / output queue capacity (reco
 #define CC_FQ_STAGES 2
 #endif
 constexpr int kFqStages = CC_FQ_STAGES;  // input tiles in flight per warp (cp.async ring)
-#ifndef CC_FQ_CONTIG
-#define CC_FQ_CONTIG 1  // each warp reads a contiguous share of the input level
+#ifndef CC_FQ_LAZYKEY
+#define CC_FQ_LAZYKEY 1  // queue records carry the parent's keysum; key(vt) is added when read
 #endif
 #ifndef CC_FQ_GATHER
 #define CC_FQ_GATHER 1  // children from a byte gather over vt's neighbour slots (NbrSlots)
@@ -536,60 +536,48 @@ __global__ void __launch_bounds__(kFBlock, 3) k_expand_fq(const LaunchArgs p, co
     const uint32_t log_p = p.pg.log_p;
     const u64 nt = (p.n_in + 31) >> 5;
     const u64 tw = (u64)gridDim.x * kFWarps;
+    const uint32_t key_sa = smem_u32(s_key);  // key(v) at key_sa + 8v (shared window)
+    auto key_of = [&](uint32_t v) {
+        u64 k;
+        asm("ld.shared.u64 %0, [%1];" : "=l"(k) : "r"(key_sa + 8 * v));
+        return k;
+    };
     WarpOut out;
     uint32_t n_in = 0, cnt1 = 0, cand1 = 0, n_next = 0, cnt2 = 0, cand2 = 0, written = 0;
     u64 hs = 0;
     uint32_t nq = 0, no = 0;  // warp-uniform queue fills
 
-#if CC_FQ_CONTIG
-    // input tile k of this warp = tile t_beg + k of its contiguous share [t_beg, t_end) of the
-    // level (static split: every tile holds 32 paths of about the same expected work); the page
-    // pointer is looked up only when the share crosses a page (tiles never straddle pages)
+    // Input: each warp reads a contiguous share [t_beg, t_end) of the level's 32-record tiles
+    // (static split: every tile holds 32 paths of about the same expected work).  Tiles never
+    // straddle pages; the page pointer is looked up only when the share enters a new page, and
+    // src advances by one tile (32 records of 8 bytes per word array) per issue.
     const u64 gw = blockIdx.x * (u64)kFWarps + (threadIdx.x >> 5);
     const u64 t_beg = nt * gw / tw, t_end = nt * (gw + 1) / tw;
-    const uint32_t tsh = log_p - 5;  // tiles per page = 2^tsh
-    uint32_t cur_pg = ~0u;
-    const char *cur_pp = nullptr;
-    auto issue = [&](u64 k) {
-        const u64 t = t_beg + k;
-        if (t < t_end) {
-            const uint32_t pg = (uint32_t)(t >> tsh);
-            if (pg != cur_pg) {
-                cur_pg = pg;
-                cur_pp = page_ptr(p.pg, p.pg.in_pages[pg]);
-            }
-            const uint32_t slot = (((uint32_t)t << 5) & ((1u << log_p) - 1)) + lane;
-            const u64 *src = (const u64 *)cur_pp + slot;
-            const int stg = (int)(k % kFqStages);
+    const uint32_t tmask = (1u << (log_p - 5)) - 1;  // tiles per page - 1
+    const u64 wstride = 8ull << log_p;                // bytes between the word arrays of a page
+    u64 t_iss = t_beg;                                // next tile to issue
+    const char *src = nullptr;                        // this lane's word-0 address in tile t_iss
+    auto locate = [&]() {
+        const char *pp = page_ptr(p.pg, p.pg.in_pages[t_iss >> (log_p - 5)]);
+        src = pp + 8 * ((((uint32_t)t_iss & tmask) << 5) + lane);
+    };
+    if (t_iss < t_end)
+        locate();
+    // one commit group per tile (empty groups past the end keep the wait counts uniform)
+    auto issue = [&](uint32_t stg) {
+        if (t_iss < t_end) {
 #pragma unroll
             for (int w = 0; w < RW; ++w)
-                cp_async8(&ws.in[stg][w][lane], src + ((u64)w << log_p));
+                cp_async8(&ws.in[stg][w][lane], src + w * wstride);
+            ++t_iss;
+            src += 32 * 8;
+            if (((uint32_t)t_iss & tmask) == 0u && t_iss < t_end)
+                locate();
         }
         cp_async_commit();
     };
-    auto tile_of = [&](u64 k) { return t_beg + k; };
-    auto more_in = [&](u64 k) { return t_beg + k < t_end; };
-#else
-    // input tile k of this warp (global tile wt0 + k * tw) -> ring stage k % kFqStages; one
-    // commit group per tile, empty groups past the end keep the wait counts uniform
-    const u64 wt0 = blockIdx.x * (u64)kFWarps + (threadIdx.x >> 5);
-    auto issue = [&](u64 k) {
-        const u64 wt = wt0 + k * tw;
-        if (wt < nt) {
-            const u64 r0 = wt << 5;
-            const char *pp = page_ptr(p.pg, p.pg.in_pages[r0 >> log_p]);
-            const uint32_t slot = (uint32_t)(r0 & ((1ull << log_p) - 1)) + lane;
-            const int stg = (int)(k % kFqStages);
-#pragma unroll
-            for (int w = 0; w < RW; ++w)
-                cp_async8(&ws.in[stg][w][lane], (const u64 *)pp + ((u64)w << log_p) + slot);
-        }
-        cp_async_commit();
-    };
-    auto tile_of = [&](u64 k) { return wt0 + k * tw; };
-    auto more_in = [&](u64 k) { return wt0 + k * tw < nt; };
-#endif
-    // write the 32 (or, at the end, fewer) records at the end of the output queue
+    // write the 32 (or, at the end, fewer) records at the end of the output queue; queue records
+    // carry their parent's keysum (CC_FQ_LAZYKEY), completed here with key(vt)
     auto flush_out = [&](uint32_t T) {
         if (T == 0 || out.dead)
             return;
@@ -605,6 +593,9 @@ __global__ void __launch_bounds__(kFBlock, 3) k_expand_fq(const LaunchArgs p, co
 #pragma unroll
             for (int w = 0; w < RW; ++w)
                 C[w] = ws.o[w][base + k];
+#if CC_FQ_LAZYKEY
+            C[NW] += key_of((uint32_t)(C[NW - 1] >> (64 - IDB)));
+#endif
             const bool lo = k < split;
             put_record<RW, true>(lo ? pp0 : pp1, lo ? s0 + k : s1 + (k - split), log_p, C, 0u);
         }
@@ -612,11 +603,12 @@ __global__ void __launch_bounds__(kFBlock, 3) k_expand_fq(const LaunchArgs p, co
     };
 
     u64 W[RW];
-    u64 kin = 0;  // next input tile of this warp
-    bool have_in = more_in(0);
+    bool have_in = t_beg < t_end;
+    uint32_t stg_rd = 0;  // ring stage of the next input round
+    u64 t_rd = t_beg;     // tile of the next input round
 #pragma unroll
     for (int k = 0; k < kFqStages - 1; ++k)
-        issue((u64)k);
+        issue((uint32_t)k);
     for (;;) {
         // ---- pick the round: children first once 32 are queued (keeps the queue bounded)
         bool child_round, valid;
@@ -633,15 +625,15 @@ __global__ void __launch_bounds__(kFBlock, 3) k_expand_fq(const LaunchArgs p, co
             nq -= take;
         } else if (have_in) {
             child_round = false;
-            cp_async_wait<kFqStages - 2>();  // tile kin has landed (this lane's own copies)
-            const int stg = (int)(kin % kFqStages);
+            cp_async_wait<kFqStages - 2>();  // tile t_rd has landed (this lane's own copies)
 #pragma unroll
             for (int w = 0; w < RW; ++w)
-                W[w] = ws.in[stg][w][lane];
-            const u64 r = (tile_of(kin) << 5) + lane;
-            issue(kin + kFqStages - 1);  // refill the stage read a round ago
-            ++kin;
-            have_in = more_in(kin);
+                W[w] = ws.in[stg_rd][w][lane];
+            const u64 r = (t_rd << 5) + lane;
+            issue((stg_rd + kFqStages - 1) % kFqStages);  // refill the stage read a round ago
+            stg_rd = (stg_rd + 1) % kFqStages;
+            ++t_rd;
+            have_in = t_rd < t_end;
             const uint32_t ids = (uint32_t)(W[NW - 1] >> (64 - 3 * IDB));
             valid = r < p.n_in && (ids & IDM) != ((ids >> IDB) & IDM);  // empty slot: v1 == v2
         } else {
@@ -661,6 +653,10 @@ __global__ void __launch_bounds__(kFBlock, 3) k_expand_fq(const LaunchArgs p, co
         if (valid) {
             const uint32_t ids = (uint32_t)(W[NW - 1] >> (64 - 3 * IDB));
             const uint32_t v1 = ids & IDM, v2 = (ids >> IDB) & IDM, vt = ids >> (2 * IDB);
+#if CC_FQ_LAZYKEY
+            if (child_round)
+                ks += key_of(vt);  // queue records carry the parent's keysum
+#endif
             u64 arow[NW], abv[NW], a1[NW], close[NW];
             lds_row<NW>(s_adj, vt, arow);
             lds_row<NW>(s_above, v2, abv);
@@ -701,7 +697,7 @@ __global__ void __launch_bounds__(kFBlock, 3) k_expand_fq(const LaunchArgs p, co
                     while (m) {
                         const int b = __ffsll((long long)m) - 1;
                         m &= m - 1;
-                        hs += mix64(ks + s_key[64 * w + b]);
+                        hs += mix64(ks + key_of(64 * w + b));
                     }
                 }
             }
@@ -743,7 +739,11 @@ __global__ void __launch_bounds__(kFBlock, 3) k_expand_fq(const LaunchArgs p, co
                     for (int w = 0; w < NW - 1; ++w)
                         dst[w][pos] = base_rec[w];
                     dst[NW - 1][pos] = base_rec[NW - 1] | ((u64)v << (64 - IDB));
-                    dst[NW][pos] = ks + s_key[v];
+#if CC_FQ_LAZYKEY
+                    dst[NW][pos] = ks;  // the child adds key(v) when it is read
+#else
+                    dst[NW][pos] = ks + key_of(v);
+#endif
                     ++pos;
                 }
         }
