@@ -448,23 +448,31 @@ constexpr int kFqStages = CC_FQ_STAGES;  // input tiles in flight per warp (cp.a
 #ifndef CC_FQ_LAZYKEY
 #define CC_FQ_LAZYKEY 1  // queue records carry the parent's keysum; key(vt) is added when read
 #endif
-#ifndef CC_FQ_GATHER
-#define CC_FQ_GATHER 1  // children from a byte gather over vt's neighbour slots (NbrSlots)
-#endif
-
 // Neighbour slots of a vertex v (max degree <= 4), for the byte gather of the extension set.
 // Every child of a path ending in v is a neighbour of v, so the <= 3 set bits of Ext (an
-// NW-word set) lie in the bytes that hold v's neighbours u_0 < u_1 < ... (CSR order).  Two
-// byte permutes move byte u_k >> 3 of Ext into byte k of one 32-bit word, a mask keeps bit
-// u_k & 7 of it:  g = (prmt(e0, e1, sel_lo) & m_lo) | (prmt(e2, e3, sel_hi) & m_hi), where
-// e0..e3 are the 32-bit quarters of Ext and (lo, hi) the slots whose byte is in bytes 0-7 /
-// 8-15.  Bit 8k + (u_k & 7) of g is set iff u_k is a child; the child's vertex is byte k of nb.
+// NW-word set, NW <= 2) lie in the bytes that hold v's neighbours u_0 < u_1 < ... (CSR order).
+// Three byte permutes move byte u_k >> 3 of Ext into byte k of one 32-bit word g:
+//   p_lo = prmt(e0, e1, sel), p_hi = prmt(e2, e3, sel)  (byte k: byte (u_k >> 3) & 7 of the half)
+//   g    = prmt(p_lo, p_hi, pick) & m                   (byte k from p_lo or p_hi)
+// where e0..e3 are the 32-bit quarters of Ext; m keeps bit u_k & 7 of byte k.  Bit 8k + (u_k & 7)
+// of g is set iff u_k is a child, and the child's vertex is byte k of nb.
 struct NbrSlots {
-    uint32_t sel;    // low 16 bits: prmt selector over (e0, e1); high 16 bits: over (e2, e3)
-    uint32_t m_lo;   // mask of the slots read from bytes 0-7
-    uint32_t m_hi;   // mask of the slots read from bytes 8-15
-    uint32_t nb;     // byte k = u_k
+    uint32_t sel;   // nibble k = (u_k >> 3) & 7
+    uint32_t pick;  // nibble k = k (u_k < 64) or 4 + k (u_k >= 64)
+    uint32_t m;     // bit 8k + (u_k & 7) for every neighbour slot k
+    uint32_t nb;    // byte k = u_k
 };
+
+__device__ __forceinline__ uint32_t prmt(uint32_t a, uint32_t b, uint32_t s)
+{
+    uint32_t d;
+    asm("prmt.b32 %0, %1, %2, %3;" : "=r"(d) : "r"(a), "r"(b), "r"(s));
+    return d;
+}
+
+#ifndef CC_FQ_FASTOUT
+#define CC_FQ_FASTOUT 1  // output reservations of exactly 32 slots in 32-aligned chunks (no split)
+#endif
 
 template <int NW>
 struct FqWarpSmem {
@@ -503,8 +511,8 @@ __global__ void __launch_bounds__(kFBlock, 3) k_expand_fq(const LaunchArgs p, co
     u64 *s_adj = smem;                          // closed rows N[v] = Adj(v) | {v}
     u64 *s_above = s_adj + n * NW;              // label gate {x : x > v}
     u64 *s_key = s_above + n * NW;              // key(v)
-    NbrSlots *s_nbx = (NbrSlots *)(s_key + ((n + 1) & ~1));  // neighbour slots (CC_FQ_GATHER)
-    char *wbase = (char *)(s_nbx + (CC_FQ_GATHER ? ((n + 1) & ~1) : 0));
+    NbrSlots *s_nbx = (NbrSlots *)(s_key + ((n + 1) & ~1));  // neighbour slots
+    char *wbase = (char *)(s_nbx + ((n + 1) & ~1));
     WS &ws = *(WS *)(wbase + (threadIdx.x >> 5) * fq_warp_bytes<NW>());
     for (int i = threadIdx.x; i < n * NW; i += kFBlock) {
         s_above[i] = above_word((uint32_t)(i / NW), i % NW);
@@ -512,23 +520,16 @@ __global__ void __launch_bounds__(kFBlock, 3) k_expand_fq(const LaunchArgs p, co
     }
     for (int i = threadIdx.x; i < n; i += kFBlock) {
         s_key[i] = p.g.key[i];
-#if CC_FQ_GATHER
         NbrSlots e{0u, 0u, 0u, 0u};
         const uint32_t r0 = p.g.rowptr[i], d = p.g.rowptr[i + 1] - r0;  // d <= 4 (host: max_deg)
         for (uint32_t k = 0; k < d; ++k) {
-            const uint32_t u = p.g.col[r0 + k], byte = u >> 3;
-            const uint32_t bit = 1u << (8 * k + (u & 7));
+            const uint32_t u = p.g.col[r0 + k];
+            e.sel |= ((u >> 3) & 7) << (4 * k);
+            e.pick |= (u < 64 ? k : 4 + k) << (4 * k);
+            e.m |= 1u << (8 * k + (u & 7));
             e.nb |= u << (8 * k);
-            if (byte < 8) {
-                e.sel |= byte << (4 * k);
-                e.m_lo |= bit;
-            } else {
-                e.sel |= (byte - 8) << (16 + 4 * k);
-                e.m_hi |= bit;
-            }
         }
         s_nbx[i] = e;
-#endif
     }
     __syncthreads();
 
@@ -578,6 +579,49 @@ __global__ void __launch_bounds__(kFBlock, 3) k_expand_fq(const LaunchArgs p, co
     };
     // write the 32 (or, at the end, fewer) records at the end of the output queue; queue records
     // carry their parent's keysum (CC_FQ_LAZYKEY), completed here with key(vt)
+#if CC_FQ_FASTOUT
+    // Output cursor: every reservation but the warp's last takes exactly 32 slots and a chunk
+    // holds 2^log_ch >= 32 slots, so a reservation never straddles a chunk: the warp keeps one
+    // pointer (this lane's word-0 address in the chunk) and the slots left in the chunk.
+    u64 *optr = nullptr;
+    uint32_t oleft = 0;
+    auto flush_out = [&](uint32_t T) {
+        if (T == 0 || out.dead)
+            return;
+        if (oleft == 0) {  // next chunk (warp-uniform)
+            u64 nb = 0;
+            if (lane == 0)
+                nb = atomicAdd(&p.sc->out_count, 1ull << log_ch);
+            nb = __shfl_sync(FULL_MASK, nb, 0);
+            if (nb + (1ull << log_ch) > p.out_cap) {
+                if (lane == 0)
+                    p.sc->err = 1;
+                out.dead = true;
+                return;
+            }
+            const u64 vo = p.out_off + nb;
+            optr = (u64 *)page_ptr(p.pg, p.pg.out_pages[vo >> log_p]) + (vo & ((1ull << log_p) - 1)) + lane;
+            oleft = 1u << log_ch;
+        }
+        written += T;
+        const uint32_t base = no - T;
+        if ((uint32_t)lane < T) {
+            u64 C[RW];
+#pragma unroll
+            for (int w = 0; w < RW; ++w)
+                C[w] = ws.o[w][base + lane];
+#if CC_FQ_LAZYKEY
+            C[NW] += key_of((uint32_t)(C[NW - 1] >> (64 - IDB)));
+#endif
+#pragma unroll
+            for (int w = 0; w < RW; ++w)
+                *(u64 *)((char *)optr + w * wstride) = C[w];
+        }
+        optr += T;
+        oleft -= T;
+        no = base;
+    };
+#else
     auto flush_out = [&](uint32_t T) {
         if (T == 0 || out.dead)
             return;
@@ -601,6 +645,7 @@ __global__ void __launch_bounds__(kFBlock, 3) k_expand_fq(const LaunchArgs p, co
         }
         no = base;
     };
+#endif
 
     u64 W[RW];
     bool have_in = t_beg < t_end;
@@ -647,9 +692,7 @@ __global__ void __launch_bounds__(kFBlock, 3) k_expand_fq(const LaunchArgs p, co
 #pragma unroll
         for (int w = 0; w < NW; ++w)
             ext[w] = 0;
-#if CC_FQ_GATHER
         uint32_t gch = 0, gnb = 0;  // children as bits of the slot gather, vt's neighbour bytes
-#endif
         if (valid) {
             const uint32_t ids = (uint32_t)(W[NW - 1] >> (64 - 3 * IDB));
             const uint32_t v1 = ids & IDM, v2 = (ids >> IDB) & IDM, vt = ids >> (2 * IDB);
@@ -661,33 +704,24 @@ __global__ void __launch_bounds__(kFBlock, 3) k_expand_fq(const LaunchArgs p, co
             lds_row<NW>(s_adj, vt, arow);
             lds_row<NW>(s_above, v2, abv);
             lds_row<NW>(s_adj, v1, a1);
-            uint32_t deg = 0;
             bool any_close = false;
-#if CC_FQ_GATHER
             const NbrSlots e = s_nbx[vt];
-            deg = __popc(e.m_lo | e.m_hi) + 1;  // |N[vt]|: one mask bit per neighbour
-#endif
+            const uint32_t deg = __popc(e.m) + 1;  // |N[vt]|: one mask bit per neighbour
 #pragma unroll
             for (int w = 0; w < NW; ++w) {
-#if !CC_FQ_GATHER
-                deg += __popcll(arow[w]);
-#endif
                 const u64 c = arow[w] & abv[w] & ~W[w];
                 close[w] = c & a1[w];
                 ext[w] = c & ~a1[w];
                 any_close |= close[w] != 0ull;
-#if !CC_FQ_GATHER
-                nc += __popcll(ext[w]);
-#endif
                 base_rec[w] = (W[w] | arow[w]) & (w == NW - 1 ? KEEP_V12 : ~0ull);  // B | N[vt]
             }
-#if CC_FQ_GATHER
-            gch = __byte_perm((uint32_t)ext[0], (uint32_t)(ext[0] >> 32), e.sel & 0xffffu) & e.m_lo;
-            if constexpr (NW == 2)
-                gch |= __byte_perm((uint32_t)ext[1], (uint32_t)(ext[1] >> 32), e.sel >> 16) & e.m_hi;
+            {
+                const uint32_t plo = prmt((uint32_t)ext[0], (uint32_t)(ext[0] >> 32), e.sel);
+                const uint32_t phi = NW == 2 ? prmt((uint32_t)ext[NW - 1], (uint32_t)(ext[NW - 1] >> 32), e.sel) : 0u;
+                gch = prmt(plo, phi, e.pick) & e.m;
+            }
             gnb = e.nb;
             nc = __popc(gch);
-#endif
             uint32_t ncl = 0;
             if (any_close && p.count) {
 #pragma unroll
@@ -728,13 +762,9 @@ __global__ void __launch_bounds__(kFBlock, 3) k_expand_fq(const LaunchArgs p, co
 #pragma unroll
             for (uint32_t c = 0; c < (uint32_t)kFMaxCh; ++c)
                 if (c < nc) {
-#if CC_FQ_GATHER
                     const uint32_t b = 31u - __clz(gch);  // highest slot bit
                     gch ^= 1u << b;
-                    const uint32_t v = __byte_perm(gnb, 0u, 0x4440u | (b >> 3));
-#else
-                    const uint32_t v = pop_lowest<NW>(ext);
-#endif
+                    const uint32_t v = prmt(gnb, 0u, 0x4440u | (b >> 3));
 #pragma unroll
                     for (int w = 0; w < NW - 1; ++w)
                         dst[w][pos] = base_rec[w];
@@ -760,6 +790,15 @@ __global__ void __launch_bounds__(kFBlock, 3) k_expand_fq(const LaunchArgs p, co
     }
     flush_out(no);  // the last partial group
     // empty slots: the unused tail of the warp's last chunk
+#if CC_FQ_FASTOUT
+    if (!out.dead && oleft) {
+        u64 *z = optr - lane;  // slot 0 of the unused tail
+        for (uint32_t k = lane; k < oleft; k += 32)
+#pragma unroll
+            for (int w = 0; w < RW; ++w)
+                *(u64 *)((char *)(z + k) + w * wstride) = 0ull;
+    }
+#else
     if (!out.dead && out.left) {
         u64 Z[RW];
 #pragma unroll
@@ -768,6 +807,7 @@ __global__ void __launch_bounds__(kFBlock, 3) k_expand_fq(const LaunchArgs p, co
         for (uint32_t k = lane; k < out.left; k += 32)
             put_record<RW, true>(out.pp, out.slot + k, log_p, Z, 0u);
     }
+#endif
     if (!p.count)
         cand1 = cand2 = 0;
     Acc a;
@@ -792,7 +832,7 @@ size_t fused_smem(int nw, int n, bool packed, int fuse)
 {
     if (fuse == 3)
         return ((size_t)n * 2 * nw + ((n + 1) & ~1)) * sizeof(u64) +
-               (CC_FQ_GATHER ? ((size_t)(n + 1) & ~(size_t)1) * sizeof(NbrSlots) : 0) +
+               ((size_t)(n + 1) & ~(size_t)1) * sizeof(NbrSlots) +
                kFWarps * (nw == 1 ? fq_warp_bytes<1>() : fq_warp_bytes<2>());
     if (nw == 1)
         return packed ? (fuse == 2 ? fused_smem_t<1, true, 2>(n) : fused_smem_t<1, true, 1>(n))
