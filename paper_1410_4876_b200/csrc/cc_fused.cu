@@ -470,6 +470,9 @@ __device__ __forceinline__ uint32_t prmt(uint32_t a, uint32_t b, uint32_t s)
     return d;
 }
 
+#ifndef CC_FQ_BRANCHFREE
+#define CC_FQ_BRANCHFREE 1  // child pushes without branches (stores of absent children to a dummy slot)
+#endif
 #ifndef CC_FQ_FASTOUT
 #define CC_FQ_FASTOUT 1  // output reservations of exactly 32 slots in 32-aligned chunks (no split)
 #endif
@@ -477,14 +480,18 @@ __device__ __forceinline__ uint32_t prmt(uint32_t a, uint32_t b, uint32_t s)
 template <int NW>
 struct FqWarpSmem {
     static constexpr int RW = NW + 1;
-    u64 q[RW][kQCap];     // child queue (F_{t+1}), SoA
-    u64 o[RW][kQCap];     // output queue (F_{t+2}), SoA
+    u64 q[RW][kQCap + 1];  // child queue (F_{t+1}), SoA; slot kQCap takes the discarded stores
+    u64 o[RW][kQCap + 1];  // output queue (F_{t+2}), SoA (branch-free pushes, CC_FQ_BRANCHFREE)
     u64 in[kFqStages][RW][32];  // input tiles, filled by cp.async (each lane copies its own record)
 };
 
 __device__ __forceinline__ void cp_async8(void *dst, const void *src)
 {
     asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(smem_u32(dst)), "l"(src) : "memory");
+}
+__device__ __forceinline__ void cp_async8_sa(uint32_t dst_sa, const void *src)
+{
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(dst_sa), "l"(src) : "memory");
 }
 __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
 template <int N>
@@ -565,11 +572,12 @@ __global__ void __launch_bounds__(kFBlock, 3) k_expand_fq(const LaunchArgs p, co
     if (t_iss < t_end)
         locate();
     // one commit group per tile (empty groups past the end keep the wait counts uniform)
+    const uint32_t in_sa = smem_u32(&ws.in[0][0][lane]);  // this lane's slot in ring stage 0
     auto issue = [&](uint32_t stg) {
         if (t_iss < t_end) {
 #pragma unroll
             for (int w = 0; w < RW; ++w)
-                cp_async8(&ws.in[stg][w][lane], src + w * wstride);
+                cp_async8_sa(in_sa + (stg * RW + w) * 32 * 8, src + w * wstride);
             ++t_iss;
             src += 32 * 8;
             if (((uint32_t)t_iss & tmask) == 0u && t_iss < t_end)
@@ -757,8 +765,24 @@ __global__ void __launch_bounds__(kFBlock, 3) k_expand_fq(const LaunchArgs p, co
             T = __popc(b0) + 2 * __popc(b1);
         }
         {
-            u64(*dst)[kQCap] = child_round ? ws.o : ws.q;
+            u64(*dst)[kQCap + 1] = child_round ? ws.o : ws.q;
             uint32_t pos = (child_round ? no : nq) + incl - nc;
+#if CC_FQ_BRANCHFREE
+            // every lane runs the three steps; a lane without a c-th child stores to slot kQCap
+#pragma unroll
+            for (uint32_t c = 0; c < (uint32_t)kFMaxCh; ++c) {
+                const uint32_t low = gch & (0u - gch);  // lowest slot bit (0 when none is left)
+                gch ^= low;
+                const uint32_t b = 31u - __clz(low);
+                const uint32_t v = prmt(gnb, 0u, 0x4440u | (b >> 3));
+                const uint32_t slot = c < nc ? pos + c : (uint32_t)kQCap;
+#pragma unroll
+                for (int w = 0; w < NW - 1; ++w)
+                    dst[w][slot] = base_rec[w];
+                dst[NW - 1][slot] = base_rec[NW - 1] | ((u64)v << (64 - IDB));
+                dst[NW][slot] = ks;  // the child adds key(v) when it is read
+            }
+#else
 #pragma unroll
             for (uint32_t c = 0; c < (uint32_t)kFMaxCh; ++c)
                 if (c < nc) {
@@ -776,6 +800,7 @@ __global__ void __launch_bounds__(kFBlock, 3) k_expand_fq(const LaunchArgs p, co
 #endif
                     ++pos;
                 }
+#endif
         }
         __syncwarp();
         if (child_round) {
