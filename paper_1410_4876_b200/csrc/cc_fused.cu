@@ -134,7 +134,7 @@ __global__ void __launch_bounds__(kFBlock, CC_FUSED_MINB) k_expand_fused(const L
     constexpr int RW = NW + 1;
     using WS = FusedWarpSmem<NW, PACK, FUSE>;
     // packed ids: a fixed width per word count (the host packs with the same, cc_host.cpp)
-    constexpr uint32_t IDB = PACK ? 5 + NW : (uint32_t)kIdBits;
+    constexpr uint32_t IDB = PACK ? (NW == 1 ? 6 : 8) : (uint32_t)kIdBits;  // cc::packed_id_bits
     constexpr uint32_t IDM = (1u << IDB) - 1;
     constexpr uint32_t V12M = (1u << (2 * IDB)) - 1;
     constexpr u64 KEEP_V12 = PACK ? ~((u64)IDM << (64 - IDB)) : ~0ull;  // packed: clears the vt field
@@ -445,9 +445,6 @@ constexpr int kQCap = 32 + kFCh1;   // child queue / output queue capacity (reco
 #define CC_FQ_STAGES 2
 #endif
 constexpr int kFqStages = CC_FQ_STAGES;  // input tiles in flight per warp (cp.async ring)
-#ifndef CC_FQ_LAZYKEY
-#define CC_FQ_LAZYKEY 1  // queue records carry the parent's keysum; key(vt) is added when read
-#endif
 // Neighbour slots of a vertex v (max degree <= 4), for the byte gather of the extension set.
 // Every child of a path ending in v is a neighbour of v, so the <= 3 set bits of Ext (an
 // NW-word set, NW <= 2) lie in the bytes that hold v's neighbours u_0 < u_1 < ... (CSR order).
@@ -470,18 +467,12 @@ __device__ __forceinline__ uint32_t prmt(uint32_t a, uint32_t b, uint32_t s)
     return d;
 }
 
-#ifndef CC_FQ_BRANCHFREE
-#define CC_FQ_BRANCHFREE 1  // child pushes without branches (stores of absent children to a dummy slot)
-#endif
-#ifndef CC_FQ_FASTOUT
-#define CC_FQ_FASTOUT 1  // output reservations of exactly 32 slots in 32-aligned chunks (no split)
-#endif
 
 template <int NW>
 struct FqWarpSmem {
     static constexpr int RW = NW + 1;
     u64 q[RW][kQCap + 1];  // child queue (F_{t+1}), SoA; slot kQCap takes the discarded stores
-    u64 o[RW][kQCap + 1];  // output queue (F_{t+2}), SoA (branch-free pushes, CC_FQ_BRANCHFREE)
+    u64 o[RW][kQCap + 1];  // output queue (F_{t+2}), SoA
     u64 in[kFqStages][RW][32];  // input tiles, filled by cp.async (each lane copies its own record)
 };
 
@@ -510,7 +501,7 @@ __global__ void __launch_bounds__(kFBlock, 3) k_expand_fq(const LaunchArgs p, co
 {
     constexpr int RW = NW + 1;
     using WS = FqWarpSmem<NW>;
-    constexpr uint32_t IDB = 5 + NW;  // packed records only (cc_host.cpp)
+    constexpr uint32_t IDB = NW == 1 ? 6 : 8;  // packed records only (cc::packed_id_bits)
     constexpr uint32_t IDM = (1u << IDB) - 1;
     constexpr u64 KEEP_V12 = ~((u64)IDM << (64 - IDB));
     extern __shared__ __align__(16) u64 smem[];
@@ -586,8 +577,7 @@ __global__ void __launch_bounds__(kFBlock, 3) k_expand_fq(const LaunchArgs p, co
         cp_async_commit();
     };
     // write the 32 (or, at the end, fewer) records at the end of the output queue; queue records
-    // carry their parent's keysum (CC_FQ_LAZYKEY), completed here with key(vt)
-#if CC_FQ_FASTOUT
+    // carry their parent's keysum, completed here with key(vt)
     // Output cursor: every reservation but the warp's last takes exactly 32 slots and a chunk
     // holds 2^log_ch >= 32 slots, so a reservation never straddles a chunk: the warp keeps one
     // pointer (this lane's word-0 address in the chunk) and the slots left in the chunk.
@@ -618,9 +608,7 @@ __global__ void __launch_bounds__(kFBlock, 3) k_expand_fq(const LaunchArgs p, co
 #pragma unroll
             for (int w = 0; w < RW; ++w)
                 C[w] = ws.o[w][base + lane];
-#if CC_FQ_LAZYKEY
             C[NW] += key_of((uint32_t)(C[NW - 1] >> (64 - IDB)));
-#endif
 #pragma unroll
             for (int w = 0; w < RW; ++w)
                 *(u64 *)((char *)optr + w * wstride) = C[w];
@@ -629,31 +617,6 @@ __global__ void __launch_bounds__(kFBlock, 3) k_expand_fq(const LaunchArgs p, co
         oleft -= T;
         no = base;
     };
-#else
-    auto flush_out = [&](uint32_t T) {
-        if (T == 0 || out.dead)
-            return;
-        char *pp0, *pp1;
-        uint32_t s0, s1, split;
-        warp_reserve(out, T, log_ch, p, pp0, s0, pp1, s1, split);
-        if (out.dead)
-            return;
-        written += T;
-        const uint32_t base = no - T;
-        for (uint32_t k = lane; k < T; k += 32) {
-            u64 C[RW];
-#pragma unroll
-            for (int w = 0; w < RW; ++w)
-                C[w] = ws.o[w][base + k];
-#if CC_FQ_LAZYKEY
-            C[NW] += key_of((uint32_t)(C[NW - 1] >> (64 - IDB)));
-#endif
-            const bool lo = k < split;
-            put_record<RW, true>(lo ? pp0 : pp1, lo ? s0 + k : s1 + (k - split), log_p, C, 0u);
-        }
-        no = base;
-    };
-#endif
 
     u64 W[RW];
     bool have_in = t_beg < t_end;
@@ -704,10 +667,8 @@ __global__ void __launch_bounds__(kFBlock, 3) k_expand_fq(const LaunchArgs p, co
         if (valid) {
             const uint32_t ids = (uint32_t)(W[NW - 1] >> (64 - 3 * IDB));
             const uint32_t v1 = ids & IDM, v2 = (ids >> IDB) & IDM, vt = ids >> (2 * IDB);
-#if CC_FQ_LAZYKEY
             if (child_round)
                 ks += key_of(vt);  // queue records carry the parent's keysum
-#endif
             u64 arow[NW], abv[NW], a1[NW], close[NW];
             lds_row<NW>(s_adj, vt, arow);
             lds_row<NW>(s_above, v2, abv);
@@ -721,7 +682,9 @@ __global__ void __launch_bounds__(kFBlock, 3) k_expand_fq(const LaunchArgs p, co
                 close[w] = c & a1[w];
                 ext[w] = c & ~a1[w];
                 any_close |= close[w] != 0ull;
-                base_rec[w] = (W[w] | arow[w]) & (w == NW - 1 ? KEEP_V12 : ~0ull);  // B | N[vt]
+                // B | N[vt]; the vt field is replaced when a child is pushed (IDB == 8: byte 3 of the
+                // upper half, overwritten by the byte permute; else cleared here)
+                base_rec[w] = (W[w] | arow[w]) & (w == NW - 1 && IDB != 8 ? KEEP_V12 : ~0ull);
             }
             {
                 const uint32_t plo = prmt((uint32_t)ext[0], (uint32_t)(ext[0] >> 32), e.sel);
@@ -767,40 +730,27 @@ __global__ void __launch_bounds__(kFBlock, 3) k_expand_fq(const LaunchArgs p, co
         {
             u64(*dst)[kQCap + 1] = child_round ? ws.o : ws.q;
             uint32_t pos = (child_round ? no : nq) + incl - nc;
-#if CC_FQ_BRANCHFREE
             // every lane runs the three steps; a lane without a c-th child stores to slot kQCap
 #pragma unroll
             for (uint32_t c = 0; c < (uint32_t)kFMaxCh; ++c) {
                 const uint32_t low = gch & (0u - gch);  // lowest slot bit (0 when none is left)
                 gch ^= low;
-                const uint32_t b = 31u - __clz(low);
+                uint32_t b;  // its position (FLO; 0xffffffff when low == 0: a dummy-slot store)
+                asm("bfind.u32 %0, %1;" : "=r"(b) : "r"(low));
                 const uint32_t v = prmt(gnb, 0u, 0x4440u | (b >> 3));
                 const uint32_t slot = c < nc ? pos + c : (uint32_t)kQCap;
 #pragma unroll
                 for (int w = 0; w < NW - 1; ++w)
                     dst[w][slot] = base_rec[w];
-                dst[NW - 1][slot] = base_rec[NW - 1] | ((u64)v << (64 - IDB));
+                if constexpr (IDB == 8) {
+                    // vt is byte 3 of the upper half: one byte permute puts v (byte k of gnb) there
+                    const uint32_t hi = prmt((uint32_t)(base_rec[NW - 1] >> 32), gnb, 0x4210u + ((b & 0x18u) << 9));
+                    dst[NW - 1][slot] = (base_rec[NW - 1] & 0xffffffffull) | ((u64)hi << 32);
+                } else {
+                    dst[NW - 1][slot] = base_rec[NW - 1] | ((u64)v << (64 - IDB));
+                }
                 dst[NW][slot] = ks;  // the child adds key(v) when it is read
             }
-#else
-#pragma unroll
-            for (uint32_t c = 0; c < (uint32_t)kFMaxCh; ++c)
-                if (c < nc) {
-                    const uint32_t b = 31u - __clz(gch);  // highest slot bit
-                    gch ^= 1u << b;
-                    const uint32_t v = prmt(gnb, 0u, 0x4440u | (b >> 3));
-#pragma unroll
-                    for (int w = 0; w < NW - 1; ++w)
-                        dst[w][pos] = base_rec[w];
-                    dst[NW - 1][pos] = base_rec[NW - 1] | ((u64)v << (64 - IDB));
-#if CC_FQ_LAZYKEY
-                    dst[NW][pos] = ks;  // the child adds key(v) when it is read
-#else
-                    dst[NW][pos] = ks + key_of(v);
-#endif
-                    ++pos;
-                }
-#endif
         }
         __syncwarp();
         if (child_round) {
@@ -815,7 +765,6 @@ __global__ void __launch_bounds__(kFBlock, 3) k_expand_fq(const LaunchArgs p, co
     }
     flush_out(no);  // the last partial group
     // empty slots: the unused tail of the warp's last chunk
-#if CC_FQ_FASTOUT
     if (!out.dead && oleft) {
         u64 *z = optr - lane;  // slot 0 of the unused tail
         for (uint32_t k = lane; k < oleft; k += 32)
@@ -823,16 +772,6 @@ __global__ void __launch_bounds__(kFBlock, 3) k_expand_fq(const LaunchArgs p, co
             for (int w = 0; w < RW; ++w)
                 *(u64 *)((char *)(z + k) + w * wstride) = 0ull;
     }
-#else
-    if (!out.dead && out.left) {
-        u64 Z[RW];
-#pragma unroll
-        for (int w = 0; w < RW; ++w)
-            Z[w] = 0;
-        for (uint32_t k = lane; k < out.left; k += 32)
-            put_record<RW, true>(out.pp, out.slot + k, log_p, Z, 0u);
-    }
-#endif
     if (!p.count)
         cand1 = cand2 = 0;
     Acc a;

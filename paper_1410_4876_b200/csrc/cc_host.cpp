@@ -785,9 +785,9 @@ static cc_status enumerate_impl(const cc_graph *cg, const cc_options *opt_in, cc
     base.root_offset = opt.root_offset;
     base.shard_index = opt.shard_index;
     base.shard_count = opt.shard_count;
-    // packed bitset records: a fixed id width per word count (6 bits for NW = 1, 7 for NW = 2; the
-    // packable graphs are the same as with ceil(log2 n)), so the kernels see it as a constant
-    base.idb = (uint32_t)(packed && !wide && nw <= 2 ? 5 + nw : cc::id_bits((int)n));
+    // packed bitset records: a fixed id width per word count (6 bits for NW = 1, 8 for NW = 2,
+    // cc::packed_id_bits), so the kernels see it as a constant
+    base.idb = (uint32_t)(packed && !wide && nw <= 2 ? cc::packed_id_bits(nw, (int)n) : cc::id_bits((int)n));
     base.packed = packed ? 1 : 0;
 
     const cc::ExpandVariant variant = (mode == cc::Mode::B && g->max_deg <= 4) ? cc::ExpandVariant::Small

@@ -139,7 +139,11 @@ inline int id_bits(int n)
         ++b;
     return b;
 }
-inline bool packable(int nw, int n) { return 64 * nw - n >= 3 * id_bits(n); }
+// id width of packed records: fixed per word count for NW <= 2 (the grid-class kernels see it as a
+// constant): 6 bits for NW = 1; 8 bits for NW = 2, so that vt is byte 3 of the last word's upper
+// half (k_expand_fq writes a child's ids with one byte permute); ceil(log2 n) otherwise
+inline int packed_id_bits(int nw, int n) { return nw == 1 ? 6 : nw == 2 ? 8 : id_bits(n); }
+inline bool packable(int nw, int n) { return 64 * nw - n >= 3 * packed_id_bits(nw, n); }
 inline int record_bytes(int nw, Mode m, bool packed) { return record_words(nw, m) * 8 + (packed ? 0 : 4); }
 
 // a.packed selects the packed-ids record variants of the B-mode kernels
