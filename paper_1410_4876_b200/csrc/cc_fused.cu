@@ -445,6 +445,10 @@ constexpr int kQCap = 32 + kFCh1;   // child queue / output queue capacity (reco
 #define CC_FQ_STAGES 2
 #endif
 constexpr int kFqStages = CC_FQ_STAGES;  // input tiles in flight per warp (cp.async ring)
+#ifndef CC_FQ_CHUNK
+#define CC_FQ_CHUNK 64
+#endif
+constexpr uint32_t kFqChunk = CC_FQ_CHUNK;  // input tiles per dynamic chunk
 // Neighbour slots of a vertex v (max degree <= 4), for the byte gather of the extension set.
 // Every child of a path ending in v is a neighbour of v, so the <= 3 set bits of Ext (an
 // NW-word set, NW <= 2) lie in the bytes that hold v's neighbours u_0 < u_1 < ... (CSR order).
@@ -546,33 +550,59 @@ __global__ void __launch_bounds__(kFBlock, 3) k_expand_fq(const LaunchArgs p, co
     u64 hs = 0;
     uint32_t nq = 0, no = 0;  // warp-uniform queue fills
 
-    // Input: each warp reads a contiguous share [t_beg, t_end) of the level's 32-record tiles
-    // (static split: every tile holds 32 paths of about the same expected work).  Tiles never
-    // straddle pages; the page pointer is looked up only when the share enters a new page, and
-    // src advances by one tile (32 records of 8 bytes per word array) per issue.
-    const u64 gw = blockIdx.x * (u64)kFWarps + (threadIdx.x >> 5);
-    const u64 t_beg = nt * gw / tw, t_end = nt * (gw + 1) / tw;
+    // Input: the level's 32-record tiles are handed out in chunks of kFqChunk consecutive tiles
+    // from a launch-wide counter (Scratch.in_next), so warps that issue faster take more chunks
+    // (a static split left ~13% of the resident warps idle on average, mostly at the end).  The
+    // next chunk's atomicAdd is issued one chunk ahead by lane 0, so its latency is hidden.
+    // Tiles never straddle pages; the page pointer is looked up only when a chunk starts or
+    // enters a new page, and src advances by one tile (32 records x 8 bytes per word array).
+    static_assert(kFqStages == 2, "the per-stage lane limits below assume a 2-stage ring");
     const uint32_t tmask = (1u << (log_p - 5)) - 1;  // tiles per page - 1
     const u64 wstride = 8ull << log_p;                // bytes between the word arrays of a page
-    u64 t_iss = t_beg;                                // next tile to issue
+    const uint32_t last_lanes = (uint32_t)(p.n_in - ((nt - 1) << 5));  // paths in the last tile
+    u64 t_iss = 0, c_end = 0;                         // next tile to issue, end of its chunk
+    u64 pend = 0;                                     // lane 0: start of the chunk after this one
     const char *src = nullptr;                        // this lane's word-0 address in tile t_iss
     auto locate = [&]() {
         const char *pp = page_ptr(p.pg, p.pg.in_pages[t_iss >> (log_p - 5)]);
         src = pp + 8 * ((((uint32_t)t_iss & tmask) << 5) + lane);
     };
-    if (t_iss < t_end)
-        locate();
-    // one commit group per tile (empty groups past the end keep the wait counts uniform)
+    {
+        u64 c0 = 0;
+        if (lane == 0) {
+            c0 = atomicAdd(&p.sc->in_next, (u64)kFqChunk);
+            pend = atomicAdd(&p.sc->in_next, (u64)kFqChunk);
+        }
+        t_iss = __shfl_sync(FULL_MASK, c0, 0);
+        c_end = t_iss + kFqChunk < nt ? t_iss + kFqChunk : nt;
+        if (t_iss < c_end)
+            locate();
+    }
+    // one commit group per tile (empty groups past the end keep the wait counts uniform);
+    // lim0 / lim1: paths in the tile of ring stage 0 / 1; infl: tiles issued and not yet read
     const uint32_t in_sa = smem_u32(&ws.in[0][0][lane]);  // this lane's slot in ring stage 0
+    uint32_t lim0 = 0, lim1 = 0, infl = 0;
     auto issue = [&](uint32_t stg) {
-        if (t_iss < t_end) {
+        if (t_iss < c_end) {
 #pragma unroll
             for (int w = 0; w < RW; ++w)
                 cp_async8_sa(in_sa + (stg * RW + w) * 32 * 8, src + w * wstride);
+            const uint32_t lim = t_iss + 1 == nt ? last_lanes : 32u;
+            lim0 = stg ? lim0 : lim;
+            lim1 = stg ? lim : lim1;
+            ++infl;
             ++t_iss;
             src += 32 * 8;
-            if (((uint32_t)t_iss & tmask) == 0u && t_iss < t_end)
+            if (t_iss == c_end) {  // chunk done: continue with the one fetched a chunk ago
+                t_iss = __shfl_sync(FULL_MASK, pend, 0);
+                if (lane == 0 && t_iss < nt)
+                    pend = atomicAdd(&p.sc->in_next, (u64)kFqChunk);
+                c_end = t_iss + kFqChunk < nt ? t_iss + kFqChunk : nt;
+                if (t_iss < c_end)
+                    locate();
+            } else if (((uint32_t)t_iss & tmask) == 0u) {
                 locate();
+            }
         }
         cp_async_commit();
     };
@@ -619,13 +649,10 @@ __global__ void __launch_bounds__(kFBlock, 3) k_expand_fq(const LaunchArgs p, co
     };
 
     u64 W[RW];
-    bool have_in = t_beg < t_end;
     uint32_t stg_rd = 0;  // ring stage of the next input round
-    u64 t_rd = t_beg;     // tile of the next input round
-#pragma unroll
-    for (int k = 0; k < kFqStages - 1; ++k)
-        issue((uint32_t)k);
+    issue(0u);
     for (;;) {
+        const bool have_in = infl > 0;
         // ---- pick the round: children first once 32 are queued (keeps the queue bounded)
         bool child_round, valid;
         if (nq >= 32 || (!have_in && nq > 0)) {
@@ -645,13 +672,12 @@ __global__ void __launch_bounds__(kFBlock, 3) k_expand_fq(const LaunchArgs p, co
 #pragma unroll
             for (int w = 0; w < RW; ++w)
                 W[w] = ws.in[stg_rd][w][lane];
-            const u64 r = (t_rd << 5) + lane;
-            issue((stg_rd + kFqStages - 1) % kFqStages);  // refill the stage read a round ago
-            stg_rd = (stg_rd + 1) % kFqStages;
-            ++t_rd;
-            have_in = t_rd < t_end;
+            const uint32_t lim = stg_rd ? lim1 : lim0;
+            --infl;
+            issue(stg_rd ^ 1u);  // refill the stage read a round ago
+            stg_rd ^= 1u;
             const uint32_t ids = (uint32_t)(W[NW - 1] >> (64 - 3 * IDB));
-            valid = r < p.n_in && (ids & IDM) != ((ids >> IDB) & IDM);  // empty slot: v1 == v2
+            valid = (uint32_t)lane < lim && (ids & IDM) != ((ids >> IDB) & IDM);  // empty slot: v1 == v2
         } else {
             break;
         }

@@ -96,6 +96,7 @@ struct Scratch {
     u64 paths_cur;               // real input paths expanded (k_expand_blocked / k_expand_fused: the
                                  // input may hold empty slots, DESIGN.md §5 "output chunks")
     u64 out_real;                // real records written (out_count also counts empty slots)
+    u64 in_next;                 // k_expand_fq: next input tile handed out (dynamic chunks)
     u64 cyc_count;               // collect-mode store counter (NOT reset per launch)
 };
 

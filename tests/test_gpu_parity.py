@@ -518,7 +518,9 @@ def test_max_len_below_three_counts_nothing(ws, K):
 FUSED_GRAPHS = [("grid5x6", I.grid(5, 6), 0), ("grid6x7", I.grid(6, 7), 0), ("grid7x8", I.grid(7, 8), 0),
                 ("grid7x10_k14", I.grid(7, 10), 14), ("grid7x10_k15", I.grid(7, 10), 15),
                 ("grid6x10_k9", I.grid(6, 10), 9), ("p8x3", I.grid(8, 3), 0), ("c40", I.cycle(40), 0),
-                ("grid6x6_k5", I.grid(6, 6), 5), ("grid6x6_k4", I.grid(6, 6), 4)]
+                ("grid6x6_k5", I.grid(6, 6), 5), ("grid6x6_k4", I.grid(6, 6), 4),
+                # n = 104 / 105: the last packable two-word graph (8-bit ids) and the first unpacked
+                ("grid8x13_k22", I.grid(8, 13), 22), ("grid7x15_k22", I.grid(7, 15), 22), ("c104", I.cycle(104), 0)]
 
 
 @pytest.mark.parametrize("fq", ["1", "0"])
@@ -544,6 +546,16 @@ def test_fused_two_level_kernel_every_level(ws, name, g, K, fq):
     # every level but the fused intermediates is written; levelsync counts each once read/written
     assert s["paths_expanded"] == int(f.sum())
     assert s["slots_moved"] >= s["bytes_alg"] // s["record_bytes"]
+
+
+@pytest.mark.parametrize("name,g,rec", [("grid8x13", I.grid(8, 13), 24), ("grid7x15", I.grid(7, 15), 28)])
+def test_packed_id_width_boundary(ws, name, g, rec):
+    """Two-word records pack v1, v2, vt as 8-bit ids above bit n iff 128 - n >= 24 (n <= 104,
+    cc::packed_id_bits); n = 105 keeps the ids in a separate u32 array.  Both equal the oracle."""
+    want = oracle.enumerate_cycles(*g, max_len=20, nthreads=NT)
+    got = gpu(g, ws, max_len=20)
+    assert_same(got, want)
+    assert got["stats"]["record_bytes"] == rec
 
 
 @pytest.mark.parametrize("kb", [1024, 4096])
