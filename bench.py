@@ -71,6 +71,21 @@ ORACLE_SAMPLE = {
 }
 
 
+def dominant_kernel(g, st):
+    """The expansion kernel that takes (almost) all of the step for this graph class."""
+    n, rowptr = g[0], np.asarray(g[1])
+    max_deg = int(np.diff(rowptr).max()) if n else 0
+    if n <= 128 and st["launches"] <= 3:
+        return "k_small_levels"  # every level in one cooperative launch (P4xP4, P8xP8)
+    if n <= 128 and max_deg <= 4 and st["record_bytes"] % 8 == 0:
+        return "k_expand_fq"  # grid class, packed records: two levels per launch
+    if n <= 128 and max_deg <= 4:
+        return "k_expand_fused"  # grid class, unpacked records
+    if n <= 512:
+        return "k_expand_blocked"
+    return "k_expand_list" if st["record_format"] == 2 else "k_expand_wide"
+
+
 def peaks():
     try:
         with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
@@ -394,8 +409,7 @@ def main():
                 "traffic_source": traffic_src, "peak_kind": peak_kind,
                 "r_alg_bytes": r_alg, "record_bytes": rec_b,
                 "achieved_moved": achieved_moved, "frac_moved": achieved_moved / peak,
-                "kernel": ("k_expand_blocked" if g[0] <= 512 else
-                           "k_expand_list" if st_last["record_format"] == 2 else "k_expand_wide"),
+                "kernel": dominant_kernel(g, st_last),
                 "expand_share_of_step": t_expand / dev_ms if dev_ms else None,
                 "records_alg_per_step": records_alg / args.steps,
                 "bytes_alg_per_step": bytes_alg / args.steps, "bytes_moved_per_step": bytes_moved / args.steps}
