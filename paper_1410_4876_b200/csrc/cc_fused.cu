@@ -27,6 +27,33 @@
 
 namespace cc {
 
+#ifdef CC_CHECKS
+__device__ unsigned int g_fq_check;  // bit c: check c failed (debug builds only)
+#define FQ_CHECK(cond, code)                        \
+    do {                                            \
+        if (!(cond))                                \
+            atomicOr(&g_fq_check, 1u << (code));    \
+    } while (0)
+#else
+#define FQ_CHECK(cond, code) \
+    do {                     \
+    } while (0)
+#endif
+
+unsigned int fused_check_flags(cudaStream_t st)
+{
+#ifdef CC_CHECKS
+    unsigned int f = 0, z = 0;
+    cudaMemcpyFromSymbolAsync(&f, g_fq_check, sizeof(f), 0, cudaMemcpyDeviceToHost, st);
+    cudaMemcpyToSymbolAsync(g_fq_check, &z, sizeof(z), 0, cudaMemcpyHostToDevice, st);
+    cudaStreamSynchronize(st);
+    return f;
+#else
+    (void)st;
+    return 0;
+#endif
+}
+
 constexpr int kFBlock = 256;             // 8 independent warps; the CTA shares the graph tables
 constexpr int kFWarps = kFBlock / 32;
 constexpr int kFMaxCh = 3;               // Delta <= 4: at most 3 children per path
@@ -549,6 +576,9 @@ __global__ void __launch_bounds__(kFBlock, 3) k_expand_fq(const LaunchArgs p, co
     uint32_t n_in = 0, cnt1 = 0, cand1 = 0, n_next = 0, cnt2 = 0, cand2 = 0, written = 0;
     u64 hs = 0;
     uint32_t nq = 0, no = 0;  // warp-uniform queue fills
+#ifdef CC_FQ_CHECK_SELFTEST
+    FQ_CHECK(blockIdx.x != 0 || threadIdx.x != 0, 7);  // negative control of the check plumbing
+#endif
 
     // Input: the level's 32-record tiles are handed out in chunks of kFqChunk consecutive tiles
     // from a launch-wide counter (Scratch.in_next), so warps that issue faster take more chunks
@@ -584,6 +614,7 @@ __global__ void __launch_bounds__(kFBlock, 3) k_expand_fq(const LaunchArgs p, co
     uint32_t lim0 = 0, lim1 = 0, infl = 0;
     auto issue = [&](uint32_t stg) {
         if (t_iss < c_end) {
+            FQ_CHECK(t_iss < nt && c_end <= nt && infl < (uint32_t)kFqStages, 2);
 #pragma unroll
             for (int w = 0; w < RW; ++w)
                 cp_async8_sa(in_sa + (stg * RW + w) * 32 * 8, src + w * wstride);
@@ -633,6 +664,7 @@ __global__ void __launch_bounds__(kFBlock, 3) k_expand_fq(const LaunchArgs p, co
         }
         written += T;
         const uint32_t base = no - T;
+        FQ_CHECK(T <= 32 && T <= oleft && no <= (uint32_t)kQCap, 4);
         if ((uint32_t)lane < T) {
             u64 C[RW];
 #pragma unroll
@@ -660,6 +692,7 @@ __global__ void __launch_bounds__(kFBlock, 3) k_expand_fq(const LaunchArgs p, co
             const uint32_t take = nq < 32 ? nq : 32;
             valid = (uint32_t)lane < take;
             const uint32_t idx = nq - take + lane;
+            FQ_CHECK(nq <= (uint32_t)kQCap, 0);
             if (valid) {
 #pragma unroll
                 for (int w = 0; w < RW; ++w)
@@ -673,6 +706,7 @@ __global__ void __launch_bounds__(kFBlock, 3) k_expand_fq(const LaunchArgs p, co
             for (int w = 0; w < RW; ++w)
                 W[w] = ws.in[stg_rd][w][lane];
             const uint32_t lim = stg_rd ? lim1 : lim0;
+            FQ_CHECK(infl >= 1 && lim >= 1 && lim <= 32, 1);
             --infl;
             issue(stg_rd ^ 1u);  // refill the stage read a round ago
             stg_rd ^= 1u;
@@ -764,6 +798,7 @@ __global__ void __launch_bounds__(kFBlock, 3) k_expand_fq(const LaunchArgs p, co
                 uint32_t b;  // its position (FLO; 0xffffffff when low == 0: a dummy-slot store)
                 asm("bfind.u32 %0, %1;" : "=r"(b) : "r"(low));
                 const uint32_t v = prmt(gnb, 0u, 0x4440u | (b >> 3));
+                FQ_CHECK(c >= nc || (pos + c < (uint32_t)kQCap && v < (uint32_t)n && (low >> b) == 1u), 3);
                 const uint32_t slot = c < nc ? pos + c : (uint32_t)kQCap;
 #pragma unroll
                 for (int w = 0; w < NW - 1; ++w)
@@ -779,6 +814,7 @@ __global__ void __launch_bounds__(kFBlock, 3) k_expand_fq(const LaunchArgs p, co
             }
         }
         __syncwarp();
+        FQ_CHECK(T <= 96 && (child_round ? no : nq) + T <= (uint32_t)kQCap, 5);
         if (child_round) {
             no += T;
             while (no >= 32 && !out.dead)

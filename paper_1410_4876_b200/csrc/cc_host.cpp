@@ -937,6 +937,10 @@ static cc_status enumerate_impl(const cc_graph *cg, const cc_options *opt_in, cc
         nvtxRangePop();
         CC_CUDA(cudaMemcpyAsync(h_sc, d_sc, sizeof(cc::Scratch), cudaMemcpyDeviceToHost, st));
         CC_CUDA(cudaStreamSynchronize(st));
+#ifdef CC_CHECKS
+        if (const unsigned int fl = cc::fused_check_flags(st))
+            return fail(CC_ERR_CUDA, "k_expand_fq bounds check failed (flags " + std::to_string(fl) + ")");
+#endif
         S.d2h_bytes += sizeof(cc::Scratch);
         S.launches++;
         float ms = 0;

@@ -190,6 +190,10 @@ cudaError_t launch_cycle_sequences(const CycleStore &c, int nw, const u64 *adj, 
 cudaError_t launch_fused(const LaunchArgs &a, int fuse, bool leaf, uint32_t log_ch, int max_warps, cudaStream_t st);
 int fused_warps_per_launch(int nw, int n, bool packed, int fuse, bool leaf, int sms);
 size_t fused_smem(int nw, int n, bool packed, int fuse);
+// Debug builds (-DCC_CHECKS, `python -m paper_1410_4876_b200.build --out ... -DCC_CHECKS`):
+// device-side bounds checks in k_expand_fq set bits of a device flag; this reads and clears it
+// (always 0 in normal builds).  The substitute for compute-sanitizer where the pool disables it.
+unsigned int fused_check_flags(cudaStream_t st);
 // dynamic shared memory of the expansion kernel for (mode, nw, n, packed)
 size_t expand_smem(Mode m, int nw, int n, bool packed);
 // Wide class (512 < n <= 2015, count mode, AoS records): which 0 = Stage 1, 1 = expand,
