@@ -755,15 +755,17 @@ __global__ void __launch_bounds__(kFBlock, 3) k_expand_fq(const LaunchArgs p, co
             nc = __popc(gch);
             uint32_t ncl = 0;
             if (any_close && p.count) {
-#pragma unroll
-                for (int w = 0; w < NW; ++w) {
-                    u64 m = close[w];
-                    ncl += __popcll(m);
-                    while (m) {
-                        const int b = __ffsll((long long)m) - 1;
-                        m &= m - 1;
-                        hs += mix64(ks + key_of(64 * w + b));
-                    }
+                // closures are neighbours of vt too: the same byte gather turns Close into <= 3
+                // slot bits of one word (one 32-bit loop instead of one 64-bit loop per word)
+                const uint32_t clo = prmt((uint32_t)close[0], (uint32_t)(close[0] >> 32), e.sel);
+                const uint32_t chi = NW == 2 ? prmt((uint32_t)close[NW - 1], (uint32_t)(close[NW - 1] >> 32), e.sel) : 0u;
+                uint32_t gcl = prmt(clo, chi, e.pick) & e.m;
+                ncl = __popc(gcl);
+                while (gcl) {
+                    uint32_t b;
+                    asm("bfind.u32 %0, %1;" : "=r"(b) : "r"(gcl));
+                    gcl ^= 1u << b;
+                    hs += mix64(ks + key_of(prmt(e.nb, 0u, 0x4440u | (b >> 3))));
                 }
             }
             if (child_round) {
