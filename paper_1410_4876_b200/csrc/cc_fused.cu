@@ -465,13 +465,13 @@ __global__ void __launch_bounds__(kFBlock, CC_FUSED_MINB) k_expand_fused(const L
 // output queue, which is written to HBM 32 records at a time (coalesced, per-warp chunks as in
 // k_expand_fused).  Child rounds run whenever the queue holds >= 32 paths, so every round but
 // the warp's last few uses all 32 lanes, and the queues stay below 32 + 96 records.  Records
-// in the queues are complete (B | N[vt] with v1, v2, vt packed, keysum): no parent references.
+// in the queues carry B | N[vt] with v1, v2, vt packed and their parent's keysum (key(vt) is
+// added when the record is popped or flushed): no parent references.  Input tiles come in
+// dynamic chunks; children and closures are found with a byte gather over vt's neighbour slots
+// (NbrSlots); pushes are branch-free (DESIGN.md §2 step 3a).
 constexpr int kQCap = 32 + kFCh1;   // child queue / output queue capacity (records)
 
-#ifndef CC_FQ_STAGES
-#define CC_FQ_STAGES 2
-#endif
-constexpr int kFqStages = CC_FQ_STAGES;  // input tiles in flight per warp (cp.async ring)
+constexpr int kFqStages = 2;  // input tiles in flight per warp (cp.async ring; 3 or 4 stages cost resident warps)
 #ifndef CC_FQ_CHUNK
 #define CC_FQ_CHUNK 64
 #endif
