@@ -472,6 +472,7 @@ __global__ void __launch_bounds__(kFBlock, CC_FUSED_MINB) k_expand_fused(const L
 constexpr int kQCap = 32 + kFCh1;   // child queue / output queue capacity (records)
 
 constexpr int kFqStages = 2;  // input tiles in flight per warp (cp.async ring; 3 or 4 stages cost resident warps)
+
 #ifndef CC_FQ_CHUNK
 #define CC_FQ_CHUNK 64
 #endif
@@ -503,7 +504,7 @@ template <int NW>
 struct FqWarpSmem {
     static constexpr int RW = NW + 1;
     u64 q[RW][kQCap + 1];  // child queue (F_{t+1}), SoA; slot kQCap takes the discarded stores
-    u64 o[RW][kQCap + 1];  // output queue (F_{t+2}), SoA
+    u64 o[RW][CC_FQ_DIRECT ? 1 : kQCap + 1];  // output queue (F_{t+2}), SoA (unused with CC_FQ_DIRECT)
     u64 in[kFqStages][RW][32];  // input tiles, filled by cp.async (each lane copies its own record)
 };
 
@@ -527,8 +528,11 @@ __host__ __device__ constexpr size_t fq_warp_bytes()
 
 // 3 CTAs per SM: shared memory (the two queues and the input ring) allows no more, so the register
 // budget may as well be 85 (P10x10: 3.18 -> 3.13 s against a 64-register cap)
+#ifndef CC_FQ_MINB
+#define CC_FQ_MINB 3
+#endif
 template <int NW>
-__global__ void __launch_bounds__(kFBlock, 3) k_expand_fq(const LaunchArgs p, const uint32_t log_ch)
+__global__ void __launch_bounds__(kFBlock, CC_FQ_MINB) k_expand_fq(const LaunchArgs p, const uint32_t log_ch)
 {
     constexpr int RW = NW + 1;
     using WS = FqWarpSmem<NW>;
@@ -565,7 +569,6 @@ __global__ void __launch_bounds__(kFBlock, 3) k_expand_fq(const LaunchArgs p, co
     const int lane = threadIdx.x & 31;
     const uint32_t log_p = p.pg.log_p;
     const u64 nt = (p.n_in + 31) >> 5;
-    const u64 tw = (u64)gridDim.x * kFWarps;
     const uint32_t key_sa = smem_u32(s_key);  // key(v) at key_sa + 8v (shared window)
     auto key_of = [&](uint32_t v) {
         u64 k;
@@ -644,6 +647,9 @@ __global__ void __launch_bounds__(kFBlock, 3) k_expand_fq(const LaunchArgs p, co
     // pointer (this lane's word-0 address in the chunk) and the slots left in the chunk.
     u64 *optr = nullptr;
     uint32_t oleft = 0;
+#if CC_FQ_DIRECT
+    u64 *ocur = nullptr;  // word 0 of the warp's next free output slot (CC_FQ_DIRECT)
+#endif
     auto flush_out = [&](uint32_t T) {
         if (T == 0 || out.dead)
             return;
@@ -779,6 +785,70 @@ __global__ void __launch_bounds__(kFBlock, 3) k_expand_fq(const LaunchArgs p, co
             }
         }
         // ---- push the children: on the child queue (input round) or the output queue
+#if CC_FQ_DIRECT
+        if (child_round) {
+            // F_{t+2}: step c writes every lane's c-th child; step c's children take the round's
+            // slots [off_c, off_c + |step c|), in lane order, so each step's stores are one
+            // contiguous run per word array.  The round reserves its T slots from the warp's
+            // chunk (a new chunk when they do not fit: [0, split) in the old one, the rest in
+            // the new one).  The records are complete: keysum + key(v).
+            uint32_t lt;
+            asm("mov.u32 %0, %%lanemask_lt;" : "=r"(lt));
+            const uint32_t bs0 = __ballot_sync(FULL_MASK, nc > 0u), bs1 = __ballot_sync(FULL_MASK, nc > 1u),
+                           bs2 = __ballot_sync(FULL_MASK, nc > 2u);
+            const uint32_t n0 = __popc(bs0), n1 = __popc(bs1);
+            const uint32_t T = n0 + n1 + __popc(bs2);
+            u64 *p0 = ocur, *p1 = ocur;
+            uint32_t split = T;
+            if (T > oleft) {  // next chunk (warp-uniform)
+                u64 nb = 0;
+                if (lane == 0)
+                    nb = atomicAdd(&p.sc->out_count, 1ull << log_ch);
+                nb = __shfl_sync(FULL_MASK, nb, 0);
+                if (nb + (1ull << log_ch) > p.out_cap) {
+                    if (lane == 0)
+                        p.sc->err = 1;
+                    out.dead = true;
+                    break;
+                }
+                const u64 vo = p.out_off + nb;
+                p1 = (u64 *)page_ptr(p.pg, p.pg.out_pages[vo >> log_p]) + (vo & ((1ull << log_p) - 1));
+                split = oleft;
+                ocur = p1 + (T - oleft);
+                oleft = (1u << log_ch) - (T - oleft);
+            } else {
+                ocur += T;
+                oleft -= T;
+            }
+            written += T;
+#pragma unroll
+            for (uint32_t c = 0; c < (uint32_t)kFMaxCh; ++c) {
+                const uint32_t low = gch & (0u - gch);  // lowest slot bit (0 when none is left)
+                gch ^= low;
+                uint32_t b;
+                asm("bfind.u32 %0, %1;" : "=r"(b) : "r"(low));
+                const uint32_t v = prmt(gnb, 0u, 0x4440u | (b >> 3));
+                if (c < nc) {
+                    const uint32_t j = (c == 0 ? 0u : c == 1 ? n0 : n0 + n1) +
+                                       __popc((c == 0 ? bs0 : c == 1 ? bs1 : bs2) & lt);
+                    FQ_CHECK(j < T && v < (uint32_t)n && (low >> b) == 1u, 6);
+                    char *dp = (char *)(j < split ? p0 + j : p1 + (j - split));
+#pragma unroll
+                    for (int w = 0; w < NW - 1; ++w)
+                        *(u64 *)(dp + w * wstride) = base_rec[w];
+                    if constexpr (IDB == 8) {
+                        const uint32_t hi = prmt((uint32_t)(base_rec[NW - 1] >> 32), gnb, 0x4210u + ((b & 0x18u) << 9));
+                        *(u64 *)(dp + (NW - 1) * wstride) = (base_rec[NW - 1] & 0xffffffffull) | ((u64)hi << 32);
+                    } else {
+                        *(u64 *)(dp + (NW - 1) * wstride) = base_rec[NW - 1] | ((u64)v << (64 - IDB));
+                    }
+                    *(u64 *)(dp + NW * wstride) = ks + key_of(v);
+                }
+            }
+            __syncwarp();
+            continue;
+        }
+#endif
         // nc <= 3 (two bits): the warp's exclusive prefix from two ballots instead of a 5-step
         // shuffle scan -- two independent votes instead of a serial chain (P10x10 3.135 -> 3.052 s)
         uint32_t incl, T;
@@ -790,7 +860,11 @@ __global__ void __launch_bounds__(kFBlock, 3) k_expand_fq(const LaunchArgs p, co
             T = __popc(b0) + 2 * __popc(b1);
         }
         {
+#if CC_FQ_DIRECT
+            u64(*dst)[kQCap + 1] = ws.q;  // child rounds stored their output above
+#else
             u64(*dst)[kQCap + 1] = child_round ? ws.o : ws.q;
+#endif
             uint32_t pos = (child_round ? no : nq) + incl - nc;
             // every lane runs the three steps; a lane without a c-th child stores to slot kQCap
 #pragma unroll
@@ -827,7 +901,11 @@ __global__ void __launch_bounds__(kFBlock, 3) k_expand_fq(const LaunchArgs p, co
         if (out.dead)
             break;
     }
+#if CC_FQ_DIRECT
+    optr = ocur + lane;  // the unused tail starts at ocur
+#else
     flush_out(no);  // the last partial group
+#endif
     // empty slots: the unused tail of the warp's last chunk
     if (!out.dead && oleft) {
         u64 *z = optr - lane;  // slot 0 of the unused tail
@@ -901,8 +979,10 @@ int fused_warps_per_launch(int nw, int n, bool packed, int fuse, bool leaf, int 
 cudaError_t launch_fused(const LaunchArgs &a, int fuse, bool leaf, uint32_t log_ch, int max_warps, cudaStream_t st)
 {
     FusedFn f = fused_kernel(a.g.nw, a.packed != 0, fuse, leaf);
-    // one reservation never needs more than one chunk: <= kFCh2 records (fuse 1 / 2), <= 32 (fuse 3)
-    if (!f || a.g.n > 128 || (1 << log_ch) < (fuse == 3 ? 32 : kFCh2) || (a.pg.log_p < log_ch) || max_warps < kFWarps)
+    // one reservation never needs more than one new chunk: <= kFCh2 records (fuse 1 / 2); fuse 3:
+    // <= 96 (a child round's output, CC_FQ_DIRECT) or exactly 32 (output-queue flushes)
+    if (!f || a.g.n > 128 || (1u << log_ch) < (fuse == 3 ? (1u << kFqMinLogChunk) : (uint32_t)kFCh2) ||
+        (a.pg.log_p < log_ch) || max_warps < kFWarps)
         return cudaErrorInvalidValue;
     const size_t smem = fused_smem(a.g.nw, a.g.n, a.packed != 0, fuse);
     cudaError_t e = cudaFuncSetAttribute((const void *)f, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);

@@ -1377,8 +1377,8 @@ static cc_status enumerate_impl(const cc_graph *cg, const cc_options *opt_in, cc
             // output chunk of the fused kernel: about 1/64 of a warp's expected output (at least
             // 512 slots, the largest single reservation, at most 4096), so the empty slots at
             // the warps' ends stay near 1% of the launch's output
-            const bool fq = fuse == 2 && packed && fq_on;  // k_expand_fq reserves 32 slots at a time
-            uint32_t log_ch = fq ? 5 : 9;
+            const bool fq = fuse == 2 && packed && fq_on;  // k_expand_fq: smaller reservations
+            uint32_t log_ch = fq ? cc::kFqMinLogChunk : 9;
             if (fuse) {
                 const double fe = L.fan > 0 && L.fan_fuse == fuse ? L.fan : (fuse == 2 ? est1(d) * est1(d + 1) : est1(d));
                 const double warps = std::max(1.0, std::min((double)fwarps(fuse, leaf), (double)c / 32.0));

@@ -190,6 +190,12 @@ cudaError_t launch_cycle_sequences(const CycleStore &c, int nw, const u64 *adj, 
 cudaError_t launch_fused(const LaunchArgs &a, int fuse, bool leaf, uint32_t log_ch, int max_warps, cudaStream_t st);
 int fused_warps_per_launch(int nw, int n, bool packed, int fuse, bool leaf, int sms);
 size_t fused_smem(int nw, int n, bool packed, int fuse);
+#ifndef CC_FQ_DIRECT
+#define CC_FQ_DIRECT 1  // k_expand_fq: children of child rounds (F_{t+2}) stored straight to HBM
+#endif
+// smallest output chunk of k_expand_fq (log2 slots): a child round reserves up to 96 slots at once
+// with direct stores (so a reservation needs at most one new chunk); output-queue flushes take 32
+constexpr uint32_t kFqMinLogChunk = CC_FQ_DIRECT ? 7 : 5;
 // Debug builds (-DCC_CHECKS, `python -m paper_1410_4876_b200.build --out ... -DCC_CHECKS`):
 // device-side bounds checks in k_expand_fq set bits of a device flag; this reads and clears it
 // (always 0 in normal builds).  The substitute for compute-sanitizer where the pool disables it.
