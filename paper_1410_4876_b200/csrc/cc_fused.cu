@@ -461,14 +461,14 @@ __global__ void __launch_bounds__(kFBlock, CC_FUSED_MINB) k_expand_fused(const L
 // k_expand_fq: the same two-level expansion (F_t -> F_{t+2}, packed records) organised as full
 // 32-lane rounds.  A round is either an input round (32 paths of F_t, straight from the input
 // tiles) or a child round (32 paths of F_{t+1} popped from the warp's child queue).  Children of
-// an input round are pushed on the queue, children of a child round (F_{t+2}) on the warp's
-// output queue, which is written to HBM 32 records at a time (coalesced, per-warp chunks as in
-// k_expand_fused).  Child rounds run whenever the queue holds >= 32 paths, so every round but
-// the warp's last few uses all 32 lanes, and the queues stay below 32 + 96 records.  Records
-// in the queues carry B | N[vt] with v1, v2, vt packed and their parent's keysum (key(vt) is
-// added when the record is popped or flushed): no parent references.  Input tiles come in
-// dynamic chunks; children and closures are found with a byte gather over vt's neighbour slots
-// (NbrSlots); pushes are branch-free (DESIGN.md §2 step 3a).
+// an input round are pushed on the queue; children of a child round (F_{t+2}) are stored straight
+// to HBM into per-warp chunks, one contiguous run per push step (CC_FQ_DIRECT; otherwise through
+// an output queue flushed 32 records at a time).  Child rounds run whenever the queue holds >= 32
+// paths, so every round but the warp's last few uses all 32 lanes, and the queue stays below
+// 32 + 96 records.  Queue records carry B | N[vt] with v1, v2, vt packed and their parent's
+// keysum (key(vt) is added when the record is popped): no parent references.  Input tiles come
+// in dynamic chunks; children and closures are found with a byte gather over vt's neighbour
+// slots (NbrSlots); pushes are branch-free (DESIGN.md §2 step 3a).
 constexpr int kQCap = 32 + kFCh1;   // child queue / output queue capacity (records)
 
 constexpr int kFqStages = 2;  // input tiles in flight per warp (cp.async ring; 3 or 4 stages cost resident warps)
@@ -526,8 +526,8 @@ __host__ __device__ constexpr size_t fq_warp_bytes()
     return (sizeof(FqWarpSmem<NW>) + 15) & ~(size_t)15;
 }
 
-// 3 CTAs per SM: shared memory (the two queues and the input ring) allows no more, so the register
-// budget may as well be 85 (P10x10: 3.18 -> 3.13 s against a 64-register cap)
+// 3 CTAs per SM and an 85-register budget: a 64-register cap (4 CTAs per SM, which shared memory
+// allows since the output queue went) measured slower (P10x10 2.087 vs 1.979 s)
 #ifndef CC_FQ_MINB
 #define CC_FQ_MINB 3
 #endif
