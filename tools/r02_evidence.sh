@@ -22,9 +22,7 @@ python tools/ncu_lines.py $O/prof_fq.src.csv 60 > $O/prof_fq.lines.txt 2>&1
 rm -f $O/prof_fq.src.csv
 python tools/traffic_json.py p10x10 $O/prof_fq.ncu-rep $O/trace_fq.csv --level 45 --kernel 'k_expand_fq<2>' \
     --record-bytes 24 --r-alg 16 --out $O/ncu_traffic.json > $O/traffic.log 2>&1
-for tool in memcheck racecheck synccheck; do
-  timeout 1500 compute-sanitizer --tool $tool --print-limit 20 python tools/sanitize_run.py > $O/sanitizer_$tool.log 2>&1
-  echo "rc=$?" >> $O/sanitizer_$tool.log
-done
+# compute-sanitizer is disabled on the pool: the bounds-checked debug build instead
+bash tools/r02_checks.sh > $O/checks.log 2>&1
 timeout 900 python tools/shard_balance.py p10x10 --shards 2 4 8 > $O/shard_balance.jsonl 2> $O/shard_balance.err
 ls -la $O
