@@ -473,10 +473,16 @@ constexpr int kQCap = 32 + kFCh1;   // child queue / output queue capacity (reco
 
 constexpr int kFqStages = 2;  // input tiles in flight per warp (cp.async ring; 3 or 4 stages cost resident warps)
 
+#ifndef CC_FQ_PAIR
+#define CC_FQ_PAIR 1  // input units of 64 records (16-byte copies, one issue per two input rounds)
+#endif
+constexpr uint32_t kFqLT = CC_FQ_PAIR ? 6 : 5;       // log2 records per input unit (ring stage)
+constexpr uint32_t kFqTile = 1u << kFqLT;            // records per input unit
+constexpr uint32_t kFqCPL = kFqTile / 32;            // consecutive records each lane copies
 #ifndef CC_FQ_CHUNK
 #define CC_FQ_CHUNK 64
 #endif
-constexpr uint32_t kFqChunk = CC_FQ_CHUNK;  // input tiles per dynamic chunk
+constexpr uint32_t kFqChunk = CC_FQ_CHUNK / kFqCPL;  // input units per dynamic chunk (2048 records)
 // Neighbour slots of a vertex v (max degree <= 4), for the byte gather of the extension set.
 // Every child of a path ending in v is a neighbour of v, so the <= 3 set bits of Ext (an
 // NW-word set, NW <= 2) lie in the bytes that hold v's neighbours u_0 < u_1 < ... (CSR order).
@@ -505,16 +511,20 @@ struct FqWarpSmem {
     static constexpr int RW = NW + 1;
     u64 q[RW][kQCap + 1];  // child queue (F_{t+1}), SoA; slot kQCap takes the discarded stores
     u64 o[RW][CC_FQ_DIRECT ? 1 : kQCap + 1];  // output queue (F_{t+2}), SoA (unused with CC_FQ_DIRECT)
-    u64 in[kFqStages][RW][32];  // input tiles, filled by cp.async (each lane copies its own record)
+    u64 in[kFqStages][RW][kFqTile];  // input units, filled by cp.async (each lane copies kFqCPL records)
 };
 
 __device__ __forceinline__ void cp_async8(void *dst, const void *src)
 {
     asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(smem_u32(dst)), "l"(src) : "memory");
 }
-__device__ __forceinline__ void cp_async8_sa(uint32_t dst_sa, const void *src)
+template <int BYTES>
+__device__ __forceinline__ void cp_async_sa(uint32_t dst_sa, const void *src)
 {
-    asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(dst_sa), "l"(src) : "memory");
+    if constexpr (BYTES == 16)
+        asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(dst_sa), "l"(src) : "memory");
+    else
+        asm volatile("cp.async.ca.shared.global [%0], [%1], %2;" ::"r"(dst_sa), "l"(src), "n"(BYTES) : "memory");
 }
 __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
 template <int N>
@@ -568,7 +578,7 @@ __global__ void __launch_bounds__(kFBlock, CC_FQ_MINB) k_expand_fq(const LaunchA
 
     const int lane = threadIdx.x & 31;
     const uint32_t log_p = p.pg.log_p;
-    const u64 nt = (p.n_in + 31) >> 5;
+    const u64 nt = (p.n_in + kFqTile - 1) >> kFqLT;  // input units
     const uint32_t key_sa = smem_u32(s_key);  // key(v) at key_sa + 8v (shared window)
     auto key_of = [&](uint32_t v) {
         u64 k;
@@ -590,15 +600,15 @@ __global__ void __launch_bounds__(kFBlock, CC_FQ_MINB) k_expand_fq(const LaunchA
     // Tiles never straddle pages; the page pointer is looked up only when a chunk starts or
     // enters a new page, and src advances by one tile (32 records x 8 bytes per word array).
     static_assert(kFqStages == 2, "the per-stage lane limits below assume a 2-stage ring");
-    const uint32_t tmask = (1u << (log_p - 5)) - 1;  // tiles per page - 1
+    const uint32_t tmask = (1u << (log_p - kFqLT)) - 1;  // units per page - 1
     const u64 wstride = 8ull << log_p;                // bytes between the word arrays of a page
-    const uint32_t last_lanes = (uint32_t)(p.n_in - ((nt - 1) << 5));  // paths in the last tile
+    const uint32_t last_recs = (uint32_t)(p.n_in - ((nt - 1) << kFqLT));  // paths in the last unit
     u64 t_iss = 0, c_end = 0;                         // next tile to issue, end of its chunk
     u64 pend = 0;                                     // lane 0: start of the chunk after this one
     const char *src = nullptr;                        // this lane's word-0 address in tile t_iss
     auto locate = [&]() {
-        const char *pp = page_ptr(p.pg, p.pg.in_pages[t_iss >> (log_p - 5)]);
-        src = pp + 8 * ((((uint32_t)t_iss & tmask) << 5) + lane);
+        const char *pp = page_ptr(p.pg, p.pg.in_pages[t_iss >> (log_p - kFqLT)]);
+        src = pp + 8 * ((((uint32_t)t_iss & tmask) << kFqLT) + kFqCPL * lane);
     };
     {
         u64 c0 = 0;
@@ -613,20 +623,20 @@ __global__ void __launch_bounds__(kFBlock, CC_FQ_MINB) k_expand_fq(const LaunchA
     }
     // one commit group per tile (empty groups past the end keep the wait counts uniform);
     // lim0 / lim1: paths in the tile of ring stage 0 / 1; infl: tiles issued and not yet read
-    const uint32_t in_sa = smem_u32(&ws.in[0][0][lane]);  // this lane's slot in ring stage 0
+    const uint32_t in_sa = smem_u32(&ws.in[0][0][kFqCPL * lane]);  // this lane's slot in ring stage 0
     uint32_t lim0 = 0, lim1 = 0, infl = 0;
     auto issue = [&](uint32_t stg) {
         if (t_iss < c_end) {
             FQ_CHECK(t_iss < nt && c_end <= nt && infl < (uint32_t)kFqStages, 2);
 #pragma unroll
             for (int w = 0; w < RW; ++w)
-                cp_async8_sa(in_sa + (stg * RW + w) * 32 * 8, src + w * wstride);
-            const uint32_t lim = t_iss + 1 == nt ? last_lanes : 32u;
+                cp_async_sa<8 * kFqCPL>(in_sa + (stg * RW + w) * kFqTile * 8, src + w * wstride);
+            const uint32_t lim = t_iss + 1 == nt ? last_recs : kFqTile;
             lim0 = stg ? lim0 : lim;
             lim1 = stg ? lim : lim1;
             ++infl;
             ++t_iss;
-            src += 32 * 8;
+            src += kFqTile * 8;
             if (t_iss == c_end) {  // chunk done: continue with the one fetched a chunk ago
                 t_iss = __shfl_sync(FULL_MASK, pend, 0);
                 if (lane == 0 && t_iss < nt)
@@ -687,10 +697,12 @@ __global__ void __launch_bounds__(kFBlock, CC_FQ_MINB) k_expand_fq(const LaunchA
     };
 
     u64 W[RW];
-    uint32_t stg_rd = 0;  // ring stage of the next input round
+    uint32_t stg_rd = 0;   // ring stage of the next input round
+    uint32_t half_rd = 0;  // which 32 records of that stage (64-record units)
+    uint32_t lim_cur = 0;  // paths in the unit being read
     issue(0u);
     for (;;) {
-        const bool have_in = infl > 0;
+        const bool have_in = infl > 0 || half_rd != 0;
         // ---- pick the round: children first once 32 are queued (keeps the queue bounded)
         bool child_round, valid;
         if (nq >= 32 || (!have_in && nq > 0)) {
@@ -707,17 +719,26 @@ __global__ void __launch_bounds__(kFBlock, CC_FQ_MINB) k_expand_fq(const LaunchA
             nq -= take;
         } else if (have_in) {
             child_round = false;
-            cp_async_wait<kFqStages - 2>();  // tile t_rd has landed (this lane's own copies)
+            if (half_rd == 0) {
+                cp_async_wait<kFqStages - 2>();  // the unit of stage stg_rd has landed
+                if (kFqCPL > 1)
+                    __syncwarp();  // ... including the records the other lanes copied
+                lim_cur = stg_rd ? lim1 : lim0;
+                FQ_CHECK(infl >= 1 && lim_cur >= 1 && lim_cur <= kFqTile, 1);
+                --infl;
+                issue(stg_rd ^ 1u);  // refill the stage read before this one
+            }
 #pragma unroll
             for (int w = 0; w < RW; ++w)
-                W[w] = ws.in[stg_rd][w][lane];
-            const uint32_t lim = stg_rd ? lim1 : lim0;
-            FQ_CHECK(infl >= 1 && lim >= 1 && lim <= 32, 1);
-            --infl;
-            issue(stg_rd ^ 1u);  // refill the stage read a round ago
-            stg_rd ^= 1u;
+                W[w] = ws.in[stg_rd][w][32 * half_rd + lane];
             const uint32_t ids = (uint32_t)(W[NW - 1] >> (64 - 3 * IDB));
-            valid = (uint32_t)lane < lim && (ids & IDM) != ((ids >> IDB) & IDM);  // empty slot: v1 == v2
+            valid = (uint32_t)lane + 32 * half_rd < lim_cur && (ids & IDM) != ((ids >> IDB) & IDM);  // empty slot: v1 == v2
+            if (kFqCPL == 1 || half_rd == 1 || lim_cur <= 32) {
+                half_rd = 0;
+                stg_rd ^= 1u;
+            } else {
+                half_rd = 1;
+            }
         } else {
             break;
         }
