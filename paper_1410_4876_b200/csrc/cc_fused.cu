@@ -482,6 +482,9 @@ constexpr uint32_t kFqCPL = kFqTile / 32;            // consecutive records each
 #ifndef CC_FQ_CHUNK
 #define CC_FQ_CHUNK 64
 #endif
+#ifndef CC_FQ_NOSPLIT
+#define CC_FQ_NOSPLIT 1  // a child round's output never straddles chunks (the old tail -> empty slots)
+#endif
 constexpr uint32_t kFqChunk = CC_FQ_CHUNK / kFqCPL;  // input units per dynamic chunk (2048 records)
 // Neighbour slots of a vertex v (max degree <= 4), for the byte gather of the extension set.
 // Every child of a path ending in v is a neighbour of v, so the <= 3 set bits of Ext (an
@@ -819,6 +822,30 @@ __global__ void __launch_bounds__(kFBlock, CC_FQ_MINB) k_expand_fq(const LaunchA
                            bs2 = __ballot_sync(FULL_MASK, nc > 2u);
             const uint32_t n0 = __popc(bs0), n1 = __popc(bs1);
             const uint32_t T = n0 + n1 + __popc(bs2);
+#if CC_FQ_NOSPLIT
+            if (T > oleft) {  // next chunk (warp-uniform); the old chunk's tail becomes empty slots
+                for (uint32_t k = lane; k < oleft; k += 32)
+#pragma unroll
+                    for (int w = 0; w < RW; ++w)
+                        *(u64 *)((char *)(ocur + k) + w * wstride) = 0ull;
+                u64 nb = 0;
+                if (lane == 0)
+                    nb = atomicAdd(&p.sc->out_count, 1ull << log_ch);
+                nb = __shfl_sync(FULL_MASK, nb, 0);
+                if (nb + (1ull << log_ch) > p.out_cap) {
+                    if (lane == 0)
+                        p.sc->err = 1;
+                    out.dead = true;
+                    break;
+                }
+                const u64 vo = p.out_off + nb;
+                ocur = (u64 *)page_ptr(p.pg, p.pg.out_pages[vo >> log_p]) + (vo & ((1ull << log_p) - 1));
+                oleft = 1u << log_ch;
+            }
+            u64 *const p0 = ocur;
+            ocur += T;
+            oleft -= T;
+#else
             u64 *p0 = ocur, *p1 = ocur;
             uint32_t split = T;
             if (T > oleft) {  // next chunk (warp-uniform)
@@ -841,6 +868,7 @@ __global__ void __launch_bounds__(kFBlock, CC_FQ_MINB) k_expand_fq(const LaunchA
                 ocur += T;
                 oleft -= T;
             }
+#endif
             written += T;
 #pragma unroll
             for (uint32_t c = 0; c < (uint32_t)kFMaxCh; ++c) {
@@ -853,7 +881,11 @@ __global__ void __launch_bounds__(kFBlock, CC_FQ_MINB) k_expand_fq(const LaunchA
                     const uint32_t j = (c == 0 ? 0u : c == 1 ? n0 : n0 + n1) +
                                        __popc((c == 0 ? bs0 : c == 1 ? bs1 : bs2) & lt);
                     FQ_CHECK(j < T && v < (uint32_t)n && (low >> b) == 1u, 6);
+#if CC_FQ_NOSPLIT
+                    char *dp = (char *)(p0 + j);
+#else
                     char *dp = (char *)(j < split ? p0 + j : p1 + (j - split));
+#endif
 #pragma unroll
                     for (int w = 0; w < NW - 1; ++w)
                         *(u64 *)(dp + w * wstride) = base_rec[w];
