@@ -482,6 +482,9 @@ constexpr uint32_t kFqCPL = kFqTile / 32;            // consecutive records each
 #ifndef CC_FQ_CHUNK
 #define CC_FQ_CHUNK 64
 #endif
+#ifndef CC_FQ_BFTEST
+#define CC_FQ_BFTEST 1  // the path test runs on every lane (invalid lanes masked), no branch
+#endif
 #ifndef CC_FQ_NOSPLIT
 #define CC_FQ_NOSPLIT 1  // a child round's output never straddles chunks (the old tail -> empty slots)
 #endif
@@ -754,8 +757,16 @@ __global__ void __launch_bounds__(kFBlock, CC_FQ_MINB) k_expand_fq(const LaunchA
         for (int w = 0; w < NW; ++w)
             ext[w] = 0;
         uint32_t gch = 0, gnb = 0;  // children as bits of the slot gather, vt's neighbour bytes
+#if CC_FQ_BFTEST
+        // branch-free: every lane runs the test; an invalid lane (no path, or an empty slot) tests
+        // vertex 0 (a safe table index) and its children, closures and statistics are masked off
+        {
+            const uint32_t ids = valid ? (uint32_t)(W[NW - 1] >> (64 - 3 * IDB)) : 0u;
+            const uint32_t vmask = valid ? ~0u : 0u;
+#else
         if (valid) {
             const uint32_t ids = (uint32_t)(W[NW - 1] >> (64 - 3 * IDB));
+#endif
             const uint32_t v1 = ids & IDM, v2 = (ids >> IDB) & IDM, vt = ids >> (2 * IDB);
             if (child_round)
                 ks += key_of(vt);  // queue records carry the parent's keysum
@@ -779,11 +790,18 @@ __global__ void __launch_bounds__(kFBlock, CC_FQ_MINB) k_expand_fq(const LaunchA
             {
                 const uint32_t plo = prmt((uint32_t)ext[0], (uint32_t)(ext[0] >> 32), e.sel);
                 const uint32_t phi = NW == 2 ? prmt((uint32_t)ext[NW - 1], (uint32_t)(ext[NW - 1] >> 32), e.sel) : 0u;
+#if CC_FQ_BFTEST
+                gch = prmt(plo, phi, e.pick) & e.m & vmask;
+#else
                 gch = prmt(plo, phi, e.pick) & e.m;
+#endif
             }
             gnb = e.nb;
             nc = __popc(gch);
             uint32_t ncl = 0;
+#if CC_FQ_BFTEST
+            any_close = any_close && valid;
+#endif
             if (any_close && p.count) {
                 // closures are neighbours of vt too: the same byte gather turns Close into <= 3
                 // slot bits of one word (one 32-bit loop instead of one 64-bit loop per word)
@@ -798,13 +816,18 @@ __global__ void __launch_bounds__(kFBlock, CC_FQ_MINB) k_expand_fq(const LaunchA
                     hs += mix64(ks + key_of(prmt(e.nb, 0u, 0x4440u | (b >> 3))));
                 }
             }
+#if CC_FQ_BFTEST
+            const uint32_t dv = (deg - 1) & vmask, nv = valid ? 1u : 0u;
+#else
+            const uint32_t dv = deg - 1, nv = 1u;
+#endif
             if (child_round) {
-                n_next++;
-                cand2 += deg - 1;
+                n_next += nv;
+                cand2 += dv;
                 cnt2 += ncl;
             } else {
-                n_in++;
-                cand1 += deg - 1;
+                n_in += nv;
+                cand1 += dv;
                 cnt1 += ncl;
             }
         }
