@@ -748,7 +748,9 @@ __global__ void __launch_bounds__(kFBlock, CC_FQ_MINB) k_expand_fq(const LaunchA
         } else {
             break;
         }
+#if !CC_FQ_DIRECT
         __syncwarp();  // queue slots just read may be overwritten by this round's pushes
+#endif
         // ---- expand the round's paths: test of Alg. 3 l.11-15 on the blocked set
         u64 ext[NW], base_rec[NW];
         uint32_t nc = 0;
@@ -924,6 +926,11 @@ __global__ void __launch_bounds__(kFBlock, CC_FQ_MINB) k_expand_fq(const LaunchA
             __syncwarp();
             continue;
         }
+#endif
+#if CC_FQ_DIRECT
+        // only input rounds write the queue: the slots popped by earlier (child) rounds must
+        // have been read by every lane before this round's pushes may overwrite them
+        __syncwarp();
 #endif
         // nc <= 3 (two bits): the warp's exclusive prefix from two ballots instead of a 5-step
         // shuffle scan -- two independent votes instead of a serial chain (P10x10 3.135 -> 3.052 s)
